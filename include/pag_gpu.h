@@ -1,0 +1,125 @@
+/*
+ * pag_gpu.h — C ABI of the B200-native PAG query path (libpag_gpu.so).
+ *
+ * Drop-in boundary for the reference's C++ search API. Each entry point
+ * names the reference interface it replaces (paths relative to the
+ * reference repo root). Plain pointers and sizes only; every call returns a
+ * status code and, on failure, leaves a thread-local message readable with
+ * pag_gpu_last_error(). Message texts are the reference's exception texts.
+ *
+ * Status codes map the reference's exception classes:
+ *   PAG_GPU_EINVAL   <- std::invalid_argument  (e.g. "K > efS",
+ *                       "query dimension mismatch",
+ *                       "zero query under cosine metric")
+ *   PAG_GPU_ERUNTIME <- std::runtime_error     (e.g. "search on empty index",
+ *                       "cannot open index: <path>", "bad index magic",
+ *                       "unsupported index version", "degree over cap in file",
+ *                       "index read failed")
+ *   PAG_GPU_ECUDA       a CUDA runtime failure (no reference counterpart)
+ */
+#ifndef PAG_GPU_H
+#define PAG_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PAG_GPU_OK 0
+#define PAG_GPU_EINVAL 1
+#define PAG_GPU_ERUNTIME 2
+#define PAG_GPU_ELOGIC 3
+#define PAG_GPU_ENOMEM 4
+#define PAG_GPU_ECUDA 5
+
+typedef struct pag_gpu_index pag_gpu_index;
+
+/* Per-query counters: proj/include/pag/routing.hpp:24-34 (SearchStats)
+ * plus edges_scanned = sum of deg(u) over expansions (algorithmic-bytes
+ * model). */
+typedef struct pag_search_stats {
+    uint64_t exact_dist_count;
+    uint64_t test_count;
+    uint64_t pass_count;
+    uint64_t visited_count;
+    uint64_t edges_scanned;
+} pag_search_stats;
+
+/* Search knobs: proj/include/pag/routing.hpp:13-22 (SearchParams).
+ * collect_pes is build-only and not part of the query path. */
+typedef struct pag_search_params {
+    uint32_t K;          /* default 10 */
+    uint32_t efS;        /* default 100 */
+    uint32_t b_override; /* 0 = max(10, K) */
+    uint8_t use_prt;     /* ablation: 0 degenerates to exact expansion */
+    uint8_t use_tfb;     /* ablation: 0 = one round with b = max(efS, b) */
+    uint8_t exact_dist;  /* 1 (default): reference-order fp32 sq_dist, bit-identical
+                            results; 0: warp-tree FMA distances (within 1e-5 rel) */
+    uint8_t reserved;
+} pag_search_params;
+
+/* Fills the reference defaults (K=10, efS=100, use_prt=use_tfb=1, exact_dist=1). */
+void pag_gpu_default_params(pag_search_params* p);
+
+/* Replaces: PagIndex load_index(const std::string&)
+ *           proj/include/pag/builder.hpp:157, proj/src/builder.cpp:434-492.
+ * Loads a PAGIDX01 v1 file, regenerates the reference family from
+ * (padded_dim, L, m, seed) (proj/src/projection.cpp:40-74) and makes the
+ * graph, per-edge codes/scalars, references and base vectors resident in
+ * HBM on every GPU of device_mask (bit i = CUDA device i; 0 = device 0).
+ * Batches are split across those GPUs (query sharding, no collective). */
+int pag_gpu_open(const char* index_path, uint32_t device_mask, pag_gpu_index** out);
+
+/* Releases every device replica (the PagIndex destructor). */
+int pag_gpu_close(pag_gpu_index* ix);
+
+/* info[0..11] = n, dim, padded_dim, L, m, M, metric (0 euclidean, 1 cosine),
+ * n_entries, seed, total_edges, n_devices, device_bytes_per_replica.
+ * Replaces the PagIndex/VectorSet accessors (builder.hpp:71-91). */
+int pag_gpu_info(const pag_gpu_index* ix, uint64_t* info, size_t n_info);
+
+/* Replaces: SearchResult search(const PagIndex&, std::span<const float> q,
+ *                                const SearchParams&, TfbState&)
+ *           proj/include/pag/routing.hpp:181-184, proj/src/routing.cpp:249-261,
+ * batched over nq queries. q: nq x dim raw host rows (padding and cosine
+ * normalisation happen exactly as routing.cpp:253-259). Outputs (host):
+ * ids/sq nq x K (the first n_out[i] entries valid, (sq, id) ascending,
+ * squared distances), n_out nq, stats nq (may be NULL). Same validation and
+ * messages as the reference; a zero query under cosine fails the call. */
+int pag_gpu_search(pag_gpu_index* ix, const float* q, uint64_t nq,
+                   const pag_search_params* params, uint32_t* ids, float* sq,
+                   uint32_t* n_out, pag_search_stats* stats);
+
+/* Same engine with every buffer already on device 0 of the handle
+ * (q_dev: nq x dim fp32, ids/sq: nq x K, n_out: nq, stats_dev: nq x 8 u32
+ * raw counters {exact,test,pass,visited,edges,status,marks,0}), launched on
+ * `stream` (a cudaStream_t; NULL = the handle's stream) without host
+ * synchronisation. For resident-input throughput measurement and for
+ * callers that keep queries on the GPU. Queries flagged with a visited-set
+ * overflow (status bit 1) are NOT retried on this path. */
+int pag_gpu_search_device(pag_gpu_index* ix, const float* q_dev, uint64_t nq,
+                          const pag_search_params* params, uint32_t* ids_dev, float* sq_dev,
+                          uint32_t* n_out_dev, uint32_t* stats_dev, void* stream);
+
+/* Replaces: GroundTruth ground_truth(const VectorSet& base,
+ *                                    const VectorSet& queries, uint32_t k_star)
+ *           proj/include/pag/bench.hpp:19, proj/src/bench.cpp:18-53,
+ * over the handle's resident base vectors: exact reference-order fp32
+ * squared distances, top-min(k, n) by (sq, id). queries: nq x dim raw host
+ * rows, zero-padded to padded_dim (no normalisation, as ground_truth reads
+ * the stored rows). ids/sq: nq x k host. */
+int pag_gpu_ground_truth(pag_gpu_index* ix, const float* queries, uint64_t nq, uint32_t k,
+                         uint32_t* ids, float* sq);
+
+/* Thread-local message of the last failing call on this thread. */
+const char* pag_gpu_last_error(void);
+
+/* Library version string. */
+const char* pag_gpu_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PAG_GPU_H */

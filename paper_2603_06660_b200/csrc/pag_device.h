@@ -1,0 +1,105 @@
+// pag_device.h — device-side data layout and kernel launch interface shared
+// by the host library (pag_host.cpp) and the kernels (pag_search.cu,
+// pag_gt.cu). No torch types; plain pointers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pagdev {
+
+// Per-query status bits written next to the counters.
+enum : uint32_t {
+    kStatusZeroCosineQuery = 1u << 0,  // routing.cpp:257 "zero query under cosine metric"
+    kStatusVisitedOverflow = 1u << 1,  // global visited table too small: host re-runs the query
+};
+
+// Per-query counters (routing.hpp:24-34 plus edges_scanned and status).
+enum : uint32_t {
+    kStatExact = 0,
+    kStatTest = 1,
+    kStatPass = 2,
+    kStatVisited = 3,
+    kStatEdges = 4,
+    kStatStatus = 5,
+    kStatWords = 8,
+};
+
+// Index resident in HBM (one replica per GPU). Layout:
+//  rows   : n x dstride fp32, dstride = round_up(padded_dim, 4), zero padded
+//  deg    : n x u32
+//  adj    : n node blocks of block_bytes, slot stride S = round_up(2M, 32):
+//           targets u32[S] | edge_norm f32[S] | cos_beta f32[S] |
+//           base_offset f32[S] | codes u32[S][cwp]   (edge-major codes)
+//  refsT  : L x sub_dim x m fp32 (reference family, transposed so one
+//           subspace's m references are contiguous per component)
+struct IndexView {
+    const float* rows;
+    const uint32_t* deg;
+    const uint8_t* adj;
+    const float* refsT;
+    const uint32_t* entries;
+    uint64_t n;
+    uint32_t dim, padded, dstride;
+    uint32_t L, m, sub_dim;
+    uint32_t slot_stride, cwp, block_bytes;
+    uint32_t n_entries;
+    uint32_t cosine;
+};
+
+// One batched search launch.
+struct SearchLaunch {
+    IndexView ix;
+    const float* queries;  // nq x dim raw rows (device)
+    uint32_t nq;
+    uint32_t K, efS, b, r_max;
+    uint32_t use_prt;
+    uint32_t exact_dist;  // 1: reference-order (bit-exact) sq_dist; 0: warp-tree
+    // outputs (device)
+    uint32_t* out_ids;    // nq x K
+    float* out_sq;        // nq x K
+    uint32_t* out_n;      // nq
+    uint32_t* out_stats;  // nq x kStatWords
+    // optional subset of query indices to run (retry path); null = all
+    const uint32_t* qlist;
+    // scheduling + scratch
+    uint32_t* qcounter;
+    uint64_t* gtab;         // per slot: 1 << gtab_log2 entries
+    uint32_t gtab_log2;
+    uint32_t* slot_epoch;   // per slot
+    uint8_t* gscratch;      // per slot: gscratch_stride bytes
+    uint64_t gscratch_stride;
+    // layout: per-warp smem and per-slot global regions (byte offsets);
+    // a region lives in smem when its *_in_smem flag is set
+    uint32_t warp_smem_bytes;
+    uint32_t off_q, off_T, off_hash, hash_log2, off_sqbuf;
+    uint32_t off_stage, stage_rows;
+    uint32_t off_W, W_in_smem;
+    uint32_t off_rf, off_rt, rings_in_smem;
+    uint32_t off_rl, rl_in_smem;
+    uint32_t off_merge, merge_in_smem;
+    uint32_t warps_per_block;
+};
+
+size_t search_kernel_smem(const SearchLaunch& L);
+cudaError_t launch_search(const SearchLaunch& L, int grid, cudaStream_t stream);
+cudaError_t search_occupancy(int warps_per_block, size_t smem_bytes, int* blocks_per_sm);
+
+// Exact brute-force ground truth (bench.cpp:18-53): reference-order fp32
+// distances, top-k by (sq, id).
+struct GtLaunch {
+    const float* base;     // n x dstride
+    uint64_t n;
+    uint32_t padded, dstride;
+    const float* queries;  // nq x dstride (already padded)
+    uint32_t nq;
+    uint32_t k;
+    uint32_t* out_ids;     // nq x k
+    float* out_sq;         // nq x k
+    float* scratch_sq;     // tiles
+    uint32_t* scratch_id;
+};
+cudaError_t launch_ground_truth(const GtLaunch& g, cudaStream_t stream);
+size_t gt_scratch_elems(uint64_t n, uint32_t nq, uint32_t k);
+
+}  // namespace pagdev

@@ -1,0 +1,844 @@
+// pag_host.cpp — host side of the B200-native PAG query path: PAGIDX01
+// ingest, reference-family regeneration, HBM residency per GPU, the batched
+// search / ground-truth drivers and the C ABI declared in include/pag_gpu.h.
+//
+// Reference interfaces mirrored (paths relative to the reference root):
+//   load_index            proj/src/builder.cpp:434-492 (+ PagIndex ctor :40-46)
+//   build_reference_set   proj/src/projection.cpp:13-74
+//   search                proj/src/routing.cpp:206-261
+//   ground_truth          proj/src/bench.cpp:18-53
+#include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/pag_gpu.h"
+#include "pag_device.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct PagError {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void throw_err(int code, std::string msg) { throw PagError{code, std::move(msg)}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw_err(PAG_GPU_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------------------
+// Reference family (projection.cpp:13-74), regenerated bit-identically with
+// the same libstdc++ engine and distribution: one mt19937_64 shared across
+// subspaces in l-major order, a fresh normal_distribution per rotation,
+// modified Gram-Schmidt in double, cast to float, vertices +e_1..+e_k then
+// -e_1..-e_k scaled by 1/sqrt(L).
+// ---------------------------------------------------------------------------
+void haar_rotation(uint32_t k, std::mt19937_64& rng, std::vector<float>& out) {
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    std::vector<double> basis(static_cast<size_t>(k) * k, 0.0), v(k);
+    for (uint32_t c = 0; c < k; ++c) {
+        for (;;) {
+            for (uint32_t r = 0; r < k; ++r) v[r] = gauss(rng);
+            for (uint32_t p = 0; p < c; ++p) {
+                const double* bp = &basis[static_cast<size_t>(p) * k];
+                double dot = 0;
+                for (uint32_t r = 0; r < k; ++r) dot += v[r] * bp[r];
+                for (uint32_t r = 0; r < k; ++r) v[r] -= dot * bp[r];
+            }
+            double nn = 0;
+            for (uint32_t r = 0; r < k; ++r) nn += v[r] * v[r];
+            nn = std::sqrt(nn);
+            if (nn > 1e-9) {
+                for (uint32_t r = 0; r < k; ++r) basis[static_cast<size_t>(c) * k + r] = v[r] / nn;
+                break;
+            }
+        }
+    }
+    out.resize(basis.size());
+    for (size_t i = 0; i < basis.size(); ++i) out[i] = static_cast<float>(basis[i]);
+}
+
+std::vector<float> reference_family(uint32_t padded, uint32_t L, uint32_t m, uint64_t seed) {
+    if (L == 0 || padded % L != 0) throw_err(PAG_GPU_EINVAL, "padded_dim not divisible by L");
+    const uint32_t sub = padded / L;
+    if (sub < 2) throw_err(PAG_GPU_EINVAL, "sub_dim < 2: cross-polytope degenerate");
+    if (m == 0 || m > 16) throw_err(PAG_GPU_EINVAL, "m must be in [1, 16] (4-bit codes)");
+    std::vector<float> refs(static_cast<size_t>(L) * m * sub, 0.0f);
+    const float scale = 1.0f / std::sqrt(static_cast<float>(L));
+    const uint32_t per_polytope = 2 * sub;
+    const uint32_t polytopes = (m + per_polytope - 1) / per_polytope;
+    std::mt19937_64 rng(seed);
+    std::vector<float> rot;
+    for (uint32_t l = 0; l < L; ++l) {
+        uint32_t j = 0;
+        for (uint32_t p = 0; p < polytopes && j < m; ++p) {
+            haar_rotation(sub, rng, rot);
+            for (uint32_t sgn = 0; sgn < 2 && j < m; ++sgn) {
+                const float s = sgn == 0 ? scale : -scale;
+                for (uint32_t c = 0; c < sub && j < m; ++c, ++j) {
+                    float* dst = &refs[(static_cast<size_t>(l) * m + j) * sub];
+                    for (uint32_t r = 0; r < sub; ++r) dst[r] = s * rot[static_cast<size_t>(c) * sub + r];
+                }
+            }
+        }
+    }
+    return refs;
+}
+
+// projection.cpp:151-166
+uint32_t default_L(uint32_t dim) {
+    uint32_t p = 1;
+    const double lim = std::sqrt(static_cast<double>(dim)) * std::sqrt(2.0);
+    while (p * 2 <= lim && p * 2 <= dim) p *= 2;
+    uint32_t hi = 1;
+    while (hi * 2 <= dim / 8) hi *= 2;
+    uint32_t lo = 8;
+    if (hi < lo) {
+        lo = hi = std::max(1u, hi);
+        while (lo * 2 <= dim / 4) lo = hi = lo * 2;
+    }
+    return std::min(std::max(p, lo), hi);
+}
+
+uint32_t ceil_log2(uint64_t x) {
+    uint32_t l = 0;
+    while ((1ull << l) < x) ++l;
+    return l;
+}
+
+// ---------------------------------------------------------------------------
+// Read-only mapping of the index file
+// ---------------------------------------------------------------------------
+struct Mapped {
+    const uint8_t* p = nullptr;
+    size_t size = 0;
+    int fd = -1;
+    ~Mapped() {
+        if (p && size) munmap(const_cast<uint8_t*>(p), size);
+        if (fd >= 0) close(fd);
+    }
+};
+
+struct Cursor {
+    const uint8_t* p;
+    size_t size, off = 0;
+    template <typename T>
+    T pod() {
+        if (off + sizeof(T) > size) throw_err(PAG_GPU_ERUNTIME, "index read failed");
+        T v;
+        std::memcpy(&v, p + off, sizeof(T));
+        off += sizeof(T);
+        return v;
+    }
+    const uint8_t* take(size_t n) {
+        if (off + n > size) throw_err(PAG_GPU_ERUNTIME, "index read failed");
+        const uint8_t* r = p + off;
+        off += n;
+        return r;
+    }
+};
+
+struct Replica {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    float* rows = nullptr;
+    uint32_t* deg = nullptr;
+    uint8_t* adj = nullptr;
+    float* refsT = nullptr;
+    uint32_t* entries = nullptr;
+    size_t bytes = 0;
+    // search scratch
+    uint64_t* gtab = nullptr;
+    uint32_t gtab_log2 = 0;
+    uint32_t* slot_epoch = nullptr;
+    size_t slots = 0;
+    uint8_t* gscratch = nullptr;
+    size_t gscratch_bytes = 0;
+    uint32_t* qcounter = nullptr;
+    // batch I/O
+    float* d_q = nullptr;
+    size_t d_q_bytes = 0;
+    uint8_t* d_out = nullptr;
+    size_t d_out_bytes = 0;
+    uint8_t* h_pin = nullptr;
+    size_t h_pin_bytes = 0;
+};
+
+template <typename T>
+void dev_alloc(T** p, size_t bytes) {
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(p), bytes ? bytes : 16), "cudaMalloc");
+}
+
+void dev_free(void* p) {
+    if (p) cudaFree(p);
+}
+
+void grow_dev(void** p, size_t* cap, size_t need) {
+    if (*cap >= need) return;
+    dev_free(*p);
+    *p = nullptr;
+    size_t n = std::max(need, *cap + *cap / 2);
+    cuda_check(cudaMalloc(p, n), "cudaMalloc");
+    *cap = n;
+}
+
+}  // namespace
+
+struct pag_gpu_index {
+    uint64_t n = 0;
+    uint32_t dim = 0, padded = 0, dstride = 0, L = 0, m = 0, M = 0, efC = 0, b_build = 0,
+             pes_flush = 0;
+    uint64_t seed = 0;
+    uint8_t metric = 0, enable_pes = 0;
+    std::vector<uint32_t> entries;
+    uint32_t maxdeg = 0, cb = 0, cwp = 0, slot_stride = 0, block_bytes = 0, sub_dim = 0;
+    uint64_t total_edges = 0;
+    std::vector<float> refs;
+    std::vector<Replica> reps;
+    std::mutex mu;
+
+    pagdev::IndexView view(const Replica& r) const {
+        pagdev::IndexView v{};
+        v.rows = r.rows;
+        v.deg = r.deg;
+        v.adj = r.adj;
+        v.refsT = r.refsT;
+        v.entries = r.entries;
+        v.n = n;
+        v.dim = dim;
+        v.padded = padded;
+        v.dstride = dstride;
+        v.L = L;
+        v.m = m;
+        v.sub_dim = sub_dim;
+        v.slot_stride = slot_stride;
+        v.cwp = cwp;
+        v.block_bytes = block_bytes;
+        v.n_entries = static_cast<uint32_t>(entries.size());
+        v.cosine = metric == 1;
+        return v;
+    }
+};
+
+namespace {
+
+void free_replica(Replica& r) {
+    cudaSetDevice(r.device);
+    for (void* p : {static_cast<void*>(r.rows), static_cast<void*>(r.deg), static_cast<void*>(r.adj),
+                    static_cast<void*>(r.refsT), static_cast<void*>(r.entries),
+                    static_cast<void*>(r.gtab), static_cast<void*>(r.slot_epoch),
+                    static_cast<void*>(r.gscratch), static_cast<void*>(r.qcounter),
+                    static_cast<void*>(r.d_q), static_cast<void*>(r.d_out)})
+        dev_free(p);
+    if (r.h_pin) cudaFreeHost(r.h_pin);
+    if (r.stream) cudaStreamDestroy(r.stream);
+    r = Replica{};
+}
+
+// ---------------------------------------------------------------------------
+// PAGIDX01 v1 ingest (builder.cpp:434-492) straight into the device layout
+// ---------------------------------------------------------------------------
+std::unique_ptr<pag_gpu_index> open_index(const char* path, uint32_t device_mask) {
+    Mapped mp;
+    mp.fd = ::open(path, O_RDONLY);
+    if (mp.fd < 0) throw_err(PAG_GPU_ERUNTIME, std::string("cannot open index: ") + path);
+    struct stat sb;
+    if (fstat(mp.fd, &sb) != 0) throw_err(PAG_GPU_ERUNTIME, std::string("cannot open index: ") + path);
+    mp.size = static_cast<size_t>(sb.st_size);
+    if (mp.size) {
+        void* p = mmap(nullptr, mp.size, PROT_READ, MAP_PRIVATE, mp.fd, 0);
+        if (p == MAP_FAILED) throw_err(PAG_GPU_ERUNTIME, std::string("cannot open index: ") + path);
+        madvise(p, mp.size, MADV_SEQUENTIAL);
+        mp.p = static_cast<const uint8_t*>(p);
+    }
+    Cursor cur{mp.p, mp.size};
+    auto ix = std::make_unique<pag_gpu_index>();
+    if (cur.pod<uint64_t>() != 0x5041474944583031ull) throw_err(PAG_GPU_ERUNTIME, "bad index magic");
+    if (cur.pod<uint32_t>() != 1u) throw_err(PAG_GPU_ERUNTIME, "unsupported index version");
+    ix->n = cur.pod<uint64_t>();
+    ix->dim = cur.pod<uint32_t>();
+    ix->padded = cur.pod<uint32_t>();
+    ix->L = cur.pod<uint32_t>();
+    ix->m = cur.pod<uint32_t>();
+    ix->M = cur.pod<uint32_t>();
+    ix->efC = cur.pod<uint32_t>();
+    ix->b_build = cur.pod<uint32_t>();
+    ix->pes_flush = cur.pod<uint32_t>();
+    ix->seed = cur.pod<uint64_t>();
+    ix->metric = cur.pod<uint8_t>();
+    ix->enable_pes = cur.pod<uint8_t>();
+    const uint32_t n_entries = cur.pod<uint32_t>();
+    ix->entries.resize(n_entries);
+    if (n_entries) std::memcpy(ix->entries.data(), cur.take(4ull * n_entries), 4ull * n_entries);
+    if (ix->n >= 0xFFFFFFFFull) throw_err(PAG_GPU_ERUNTIME, "index too large for 32-bit ids");
+    // PagIndex constructor: VectorSet(dim, padded) then repad(L) (builder.cpp:40-46)
+    if (ix->padded < ix->dim) throw_err(PAG_GPU_EINVAL, "padded_dim < dim");
+    if (ix->L == 0) ix->L = default_L(ix->dim);
+    if (((ix->dim + ix->L - 1) / ix->L) * ix->L != ix->padded)
+        throw_err(PAG_GPU_ERUNTIME, "padded_dim mismatch on load");
+    ix->refs = reference_family(ix->padded, ix->L, ix->m, ix->seed);
+    ix->sub_dim = ix->padded / ix->L;
+    ix->dstride = (ix->padded + 3u) & ~3u;
+    ix->maxdeg = 2 * ix->M;
+    ix->cb = (ix->L + 1) / 2;
+    ix->cwp = 1;
+    while (ix->cwp * 4 < ix->cb) ix->cwp *= 2;
+    ix->slot_stride = std::max(32u, (ix->maxdeg + 31u) & ~31u);
+    ix->block_bytes = ix->slot_stride * (16u + 4u * ix->cwp);
+
+    std::vector<int> devs;
+    if (device_mask == 0) device_mask = 1;
+    int ndev = 0;
+    cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    for (int d = 0; d < 32; ++d)
+        if (device_mask & (1u << d)) {
+            if (d >= ndev) throw_err(PAG_GPU_EINVAL, "device_mask names a missing GPU");
+            devs.push_back(d);
+        }
+
+    const uint64_t n = ix->n;
+    const size_t row_bytes = 4ull * ix->dstride;
+    for (int d : devs) {
+        Replica r;
+        r.device = d;
+        cuda_check(cudaSetDevice(d), "cudaSetDevice");
+        cudaDeviceGetAttribute(&r.num_sms, cudaDevAttrMultiProcessorCount, d);
+        cuda_check(cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        dev_alloc(&r.rows, n * row_bytes);
+        dev_alloc(&r.deg, 4ull * n);
+        dev_alloc(&r.adj, static_cast<size_t>(n) * ix->block_bytes);
+        dev_alloc(&r.refsT, 4ull * ix->refs.size());
+        dev_alloc(&r.entries, 4ull * std::max<size_t>(1, n_entries));
+        dev_alloc(&r.qcounter, 16);
+        r.bytes = n * row_bytes + 4ull * n + static_cast<size_t>(n) * ix->block_bytes +
+                  4ull * ix->refs.size();
+        ix->reps.push_back(r);
+    }
+
+    // refs transposed: refsT[(l*sub + c)*m + j] = refs[(l*m + j)*sub + c]
+    {
+        const uint32_t L = ix->L, m = ix->m, sub = ix->sub_dim;
+        std::vector<float> rt(ix->refs.size());
+        for (uint32_t l = 0; l < L; ++l)
+            for (uint32_t j = 0; j < m; ++j)
+                for (uint32_t c = 0; c < sub; ++c)
+                    rt[(static_cast<size_t>(l) * sub + c) * m + j] =
+                        ix->refs[(static_cast<size_t>(l) * m + j) * sub + c];
+        for (auto& r : ix->reps) {
+            cudaSetDevice(r.device);
+            cuda_check(cudaMemcpy(r.refsT, rt.data(), 4 * rt.size(), cudaMemcpyHostToDevice), "H2D refs");
+            if (n_entries)
+                cuda_check(cudaMemcpy(r.entries, ix->entries.data(), 4ull * n_entries,
+                                      cudaMemcpyHostToDevice),
+                           "H2D entries");
+        }
+    }
+
+    // adjacency: stream node blocks through two pinned staging buffers
+    const size_t CH = 1u << 16;  // nodes per chunk
+    const size_t chunk_bytes = CH * ix->block_bytes;
+    uint8_t* stage[2] = {nullptr, nullptr};
+    uint32_t* dstage[2] = {nullptr, nullptr};
+    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&stage[0]), chunk_bytes, 0), "cudaHostAlloc");
+    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&stage[1]), chunk_bytes, 0), "cudaHostAlloc");
+    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&dstage[0]), CH * 4, 0), "cudaHostAlloc");
+    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&dstage[1]), CH * 4, 0), "cudaHostAlloc");
+    struct Free {
+        uint8_t** s;
+        uint32_t** d;
+        ~Free() {
+            for (int i = 0; i < 2; ++i) {
+                if (s[i]) cudaFreeHost(s[i]);
+                if (d[i]) cudaFreeHost(d[i]);
+            }
+        }
+    } fr{stage, dstage};
+    const uint32_t S = ix->slot_stride, cb = ix->cb, cwp = ix->cwp;
+    const size_t rec = 4 + cb + 12;
+    int buf = 0;
+    for (uint64_t u0 = 0; u0 < n; u0 += CH) {
+        const uint64_t cnt = std::min<uint64_t>(CH, n - u0);
+        for (auto& r : ix->reps) cudaStreamSynchronize(r.stream);  // buffer reuse
+        uint8_t* blk0 = stage[buf];
+        uint32_t* dg = dstage[buf];
+        std::memset(blk0, 0, cnt * ix->block_bytes);
+        for (uint64_t i = 0; i < cnt; ++i) {
+            const uint32_t deg = cur.pod<uint32_t>();
+            if (deg > ix->maxdeg) throw_err(PAG_GPU_ERUNTIME, "degree over cap in file");
+            dg[i] = deg;
+            ix->total_edges += deg;
+            const uint8_t* e = cur.take(rec * deg);
+            uint8_t* blk = blk0 + i * ix->block_bytes;
+            uint32_t* tg = reinterpret_cast<uint32_t*>(blk);
+            float* en = reinterpret_cast<float*>(blk + 4u * S);
+            float* cbeta = reinterpret_cast<float*>(blk + 8u * S);
+            float* bo = reinterpret_cast<float*>(blk + 12u * S);
+            uint8_t* codes = blk + 16u * S;
+            for (uint32_t j = 0; j < deg; ++j, e += rec) {
+                uint32_t t;
+                std::memcpy(&t, e, 4);
+                if (t >= n) throw_err(PAG_GPU_ERUNTIME, "edge target out of range in file");
+                tg[j] = t;
+                std::memcpy(codes + static_cast<size_t>(j) * 4 * cwp, e + 4, cb);
+                std::memcpy(&cbeta[j], e + 4 + cb, 4);
+                std::memcpy(&en[j], e + 8 + cb, 4);
+                std::memcpy(&bo[j], e + 12 + cb, 4);
+            }
+        }
+        for (auto& r : ix->reps) {
+            cudaSetDevice(r.device);
+            cuda_check(cudaMemcpyAsync(r.adj + u0 * ix->block_bytes, blk0, cnt * ix->block_bytes,
+                                       cudaMemcpyHostToDevice, r.stream),
+                       "H2D adjacency");
+            cuda_check(cudaMemcpyAsync(r.deg + u0, dg, cnt * 4, cudaMemcpyHostToDevice, r.stream),
+                       "H2D degrees");
+        }
+        buf ^= 1;
+    }
+    for (auto& r : ix->reps) cuda_check(cudaStreamSynchronize(r.stream), "adjacency upload");
+
+    // rows (n x padded fp32), restrided to dstride with zero padding
+    {
+        const uint8_t* rows = cur.take(4ull * ix->padded * n);
+        cur.take(4ull * n);  // cached norms: read (presence checked) but not needed on device
+        const size_t RCH = std::max<size_t>(1, chunk_bytes / row_bytes);
+        buf = 0;
+        for (uint64_t i0 = 0; i0 < n; i0 += RCH) {
+            const uint64_t cnt = std::min<uint64_t>(RCH, n - i0);
+            for (auto& r : ix->reps) cudaStreamSynchronize(r.stream);
+            uint8_t* st = stage[buf];
+            if (ix->dstride == ix->padded) {
+                std::memcpy(st, rows + i0 * row_bytes, cnt * row_bytes);
+            } else {
+                std::memset(st, 0, cnt * row_bytes);
+                for (uint64_t i = 0; i < cnt; ++i)
+                    std::memcpy(st + i * row_bytes, rows + (i0 + i) * 4ull * ix->padded, 4ull * ix->padded);
+            }
+            for (auto& r : ix->reps) {
+                cudaSetDevice(r.device);
+                cuda_check(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(r.rows) + i0 * row_bytes, st,
+                                           cnt * row_bytes, cudaMemcpyHostToDevice, r.stream),
+                           "H2D rows");
+            }
+            buf ^= 1;
+        }
+        for (auto& r : ix->reps) cuda_check(cudaStreamSynchronize(r.stream), "rows upload");
+    }
+    return ix;
+}
+
+// ---------------------------------------------------------------------------
+// Search driver (routing.cpp:206-261 per query, batched)
+// ---------------------------------------------------------------------------
+struct Plan {
+    pagdev::SearchLaunch L{};
+    size_t gscratch_stride = 0;
+    int grid = 0;
+};
+
+constexpr int kWarpsPerBlock = 4;
+constexpr uint32_t kWarpSmemBudget = 20 * 1024;
+
+uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
+
+Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_params& p, uint32_t nq,
+               uint32_t gt_log2_min) {
+    Plan pl;
+    auto& L = pl.L;
+    const uint32_t bdef = p.b_override ? p.b_override : std::max(10u, p.K);
+    L.b = p.use_tfb ? bdef : std::max(p.efS, bdef);
+    L.r_max = p.use_tfb ? (p.efS + L.b - 1) / L.b : 1u;
+    L.K = p.K;
+    L.efS = p.efS;
+    L.use_prt = p.use_prt;
+    L.exact_dist = p.exact_dist;
+    L.nq = nq;
+    L.ix = ix.view(r);
+    L.warps_per_block = kWarpsPerBlock;
+    L.stage_rows = 8;
+    L.hash_log2 = p.efS <= 200 ? 10 : 11;
+    const uint32_t b = L.b, capr = std::max(1u, p.efS);
+    // fixed smem regions
+    uint32_t off = 0;
+    L.off_q = off;
+    off = align16(off + 4 * ix.dstride);
+    L.off_T = off;
+    off = align16(off + 4 * ix.L * ix.m);
+    L.off_hash = off;
+    off = align16(off + (4u << L.hash_log2));
+    L.off_sqbuf = off;
+    off = align16(off + 256);
+    L.off_stage = off;
+    off = align16(off + 4 * 132 * L.stage_rows);
+    // movable regions: W (12b), rings (24b), R_L (24 capr), merge (48b)
+    const uint64_t szW = align16(12 * b), szR = align16(24 * b), szRL = align16(24 * capr),
+                   szM = align16(48 * b);
+    bool w_s = true, r_s = true, rl_s = true, m_s = true;
+    auto total = [&]() {
+        return off + (w_s ? szW : 0) + (r_s ? szR : 0) + (rl_s ? szRL : 0) + (m_s ? szM : 0);
+    };
+    if (total() > kWarpSmemBudget) rl_s = false;
+    if (total() > kWarpSmemBudget) m_s = false;
+    if (total() > kWarpSmemBudget) r_s = false;
+    if (total() > kWarpSmemBudget) w_s = false;
+    uint64_t goff = 0;
+    auto place = [&](bool in_smem, uint64_t sz, uint32_t* o, uint32_t* flag) {
+        *flag = in_smem;
+        if (in_smem) {
+            *o = off;
+            off = align16(static_cast<uint32_t>(off + sz));
+        } else {
+            *o = static_cast<uint32_t>(goff);
+            goff = (goff + sz + 255) & ~255ull;
+        }
+    };
+    place(w_s, szW, &L.off_W, &L.W_in_smem);
+    uint32_t dummy;
+    place(r_s, szR, &L.off_rf, &L.rings_in_smem);
+    L.off_rt = L.off_rf + 12 * b;
+    (void)dummy;
+    place(rl_s, szRL, &L.off_rl, &L.rl_in_smem);
+    place(m_s, szM, &L.off_merge, &L.merge_in_smem);
+    L.warp_smem_bytes = align16(off);
+    pl.gscratch_stride = std::max<uint64_t>(256, goff);
+    L.gscratch_stride = pl.gscratch_stride;
+    // per-slot HBM visited table
+    uint64_t want = 2ull * (16ull * p.efS + 512ull);
+    L.gtab_log2 = std::max<uint32_t>(std::max<uint32_t>(12, ceil_log2(want)), gt_log2_min);
+    int bps = 0;
+    size_t smem = static_cast<size_t>(L.warp_smem_bytes) * kWarpsPerBlock;
+    cuda_check(pagdev::search_occupancy(kWarpsPerBlock, smem, &bps), "occupancy");
+    if (bps <= 0) throw_err(PAG_GPU_ERUNTIME, "search configuration does not fit on the GPU");
+    const int want_blocks = static_cast<int>((nq + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    pl.grid = std::max(1, std::min(r.num_sms * bps, want_blocks));
+    return pl;
+}
+
+void ensure_scratch(Replica& r, Plan& pl) {
+    auto& L = pl.L;
+    const size_t slots = static_cast<size_t>(pl.grid) * kWarpsPerBlock;
+    if (slots > r.slots || L.gtab_log2 != r.gtab_log2) {
+        const size_t ns = std::max(slots, r.slots);
+        dev_free(r.gtab);
+        dev_free(r.slot_epoch);
+        r.gtab = nullptr;
+        r.slot_epoch = nullptr;
+        dev_alloc(&r.gtab, (ns << L.gtab_log2) * 8);
+        dev_alloc(&r.slot_epoch, ns * 4);
+        cuda_check(cudaMemsetAsync(r.gtab, 0, (ns << L.gtab_log2) * 8, r.stream), "memset");
+        cuda_check(cudaMemsetAsync(r.slot_epoch, 0, ns * 4, r.stream), "memset");
+        r.slots = ns;
+        r.gtab_log2 = L.gtab_log2;
+    }
+    grow_dev(reinterpret_cast<void**>(&r.gscratch), &r.gscratch_bytes, r.slots * pl.gscratch_stride);
+    L.gtab = r.gtab;
+    L.slot_epoch = r.slot_epoch;
+    L.gscratch = r.gscratch;
+    L.qcounter = r.qcounter;
+}
+
+void validate_params(const pag_gpu_index& ix, const pag_search_params& p) {
+    if (ix.n == 0) throw_err(PAG_GPU_ERUNTIME, "search on empty index");  // routing.cpp:208
+    if (p.K > p.efS) throw_err(PAG_GPU_EINVAL, "K > efS");                // routing.cpp:209
+}
+
+// Runs nq queries already on the replica's device. Device buffers:
+// q (nq x dim), ids/sq (nq x K), n_out (nq), stats (nq x 8). qlist optional.
+void run_search(pag_gpu_index& ix, Replica& r, const pag_search_params& p, const float* q_dev,
+                uint32_t nq, const uint32_t* qlist, uint32_t* ids, float* sq, uint32_t* n_out,
+                uint32_t* stats, cudaStream_t stream, uint32_t gt_log2_min) {
+    if (nq == 0) return;
+    Plan pl = make_plan(ix, r, p, nq, gt_log2_min);
+    ensure_scratch(r, pl);
+    auto& L = pl.L;
+    L.queries = q_dev;
+    L.qlist = qlist;
+    L.out_ids = ids;
+    L.out_sq = sq;
+    L.out_n = n_out;
+    L.out_stats = stats;
+    cuda_check(cudaMemsetAsync(r.qcounter, 0, 4, stream), "memset");
+    cuda_check(pagdev::launch_search(L, pl.grid, stream), "search kernel launch");
+}
+
+void search_on_replica(pag_gpu_index& ix, Replica& r, const pag_search_params& p, const float* q,
+                       uint64_t nq, uint32_t* ids, float* sq, uint32_t* n_out,
+                       pag_search_stats* stats, uint32_t* status_or) {
+    cuda_check(cudaSetDevice(r.device), "cudaSetDevice");
+    if (nq == 0) return;
+    const uint32_t K = p.K;
+    const size_t qb = 4ull * nq * ix.dim;
+    const size_t ob_ids = 4ull * nq * std::max(1u, K), ob_n = 4ull * nq,
+                 ob_st = 4ull * nq * pagdev::kStatWords, ob_list = 4ull * nq;
+    grow_dev(reinterpret_cast<void**>(&r.d_q), &r.d_q_bytes, qb);
+    grow_dev(reinterpret_cast<void**>(&r.d_out), &r.d_out_bytes, 2 * ob_ids + ob_n + ob_st + ob_list);
+    uint32_t* d_ids = reinterpret_cast<uint32_t*>(r.d_out);
+    float* d_sq = reinterpret_cast<float*>(r.d_out + ob_ids);
+    uint32_t* d_n = reinterpret_cast<uint32_t*>(r.d_out + 2 * ob_ids);
+    uint32_t* d_st = reinterpret_cast<uint32_t*>(r.d_out + 2 * ob_ids + ob_n);
+    uint32_t* d_list = reinterpret_cast<uint32_t*>(r.d_out + 2 * ob_ids + ob_n + ob_st);
+    cuda_check(cudaMemcpyAsync(r.d_q, q, qb, cudaMemcpyHostToDevice, r.stream), "H2D queries");
+    run_search(ix, r, p, r.d_q, static_cast<uint32_t>(nq), nullptr, d_ids, d_sq, d_n, d_st, r.stream, 0);
+    std::vector<uint32_t> st(nq * pagdev::kStatWords);
+    cuda_check(cudaMemcpyAsync(st.data(), d_st, ob_st, cudaMemcpyDeviceToHost, r.stream), "D2H stats");
+    cuda_check(cudaStreamSynchronize(r.stream), "search");
+    // visited-set overflow: re-run those queries with a 4x larger HBM table
+    uint32_t grow = 2;
+    for (int attempt = 0; attempt < 6; ++attempt) {
+        std::vector<uint32_t> redo;
+        for (uint64_t i = 0; i < nq; ++i)
+            if (st[i * pagdev::kStatWords + pagdev::kStatStatus] & pagdev::kStatusVisitedOverflow)
+                redo.push_back(static_cast<uint32_t>(i));
+        if (redo.empty()) break;
+        cuda_check(cudaMemcpyAsync(d_list, redo.data(), 4 * redo.size(), cudaMemcpyHostToDevice, r.stream),
+                   "H2D retry list");
+        run_search(ix, r, p, r.d_q, static_cast<uint32_t>(redo.size()), d_list, d_ids, d_sq, d_n, d_st,
+                   r.stream, r.gtab_log2 + grow);
+        cuda_check(cudaMemcpyAsync(st.data(), d_st, ob_st, cudaMemcpyDeviceToHost, r.stream), "D2H stats");
+        cuda_check(cudaStreamSynchronize(r.stream), "search retry");
+    }
+    if (K) {
+        cuda_check(cudaMemcpyAsync(ids, d_ids, 4ull * nq * K, cudaMemcpyDeviceToHost, r.stream), "D2H ids");
+        cuda_check(cudaMemcpyAsync(sq, d_sq, 4ull * nq * K, cudaMemcpyDeviceToHost, r.stream), "D2H sq");
+    }
+    cuda_check(cudaMemcpyAsync(n_out, d_n, ob_n, cudaMemcpyDeviceToHost, r.stream), "D2H n_out");
+    cuda_check(cudaStreamSynchronize(r.stream), "D2H");
+    uint32_t so = 0;
+    for (uint64_t i = 0; i < nq; ++i) {
+        const uint32_t* s = &st[i * pagdev::kStatWords];
+        so |= s[pagdev::kStatStatus];
+        if (stats) {
+            stats[i].exact_dist_count = s[pagdev::kStatExact];
+            stats[i].test_count = s[pagdev::kStatTest];
+            stats[i].pass_count = s[pagdev::kStatPass];
+            stats[i].visited_count = s[pagdev::kStatVisited];
+            stats[i].edges_scanned = s[pagdev::kStatEdges];
+        }
+    }
+    *status_or = so;
+}
+
+// ---------------------------------------------------------------------------
+// Ground truth driver
+// ---------------------------------------------------------------------------
+void ground_truth_on_replica(pag_gpu_index& ix, Replica& r, const float* q, uint64_t nq, uint32_t k,
+                             uint32_t* ids, float* sq) {
+    cuda_check(cudaSetDevice(r.device), "cudaSetDevice");
+    if (nq == 0 || k == 0) return;
+    const uint32_t kk = static_cast<uint32_t>(std::min<uint64_t>(k, ix.n));
+    std::vector<float> qp(nq * ix.dstride, 0.0f);
+    for (uint64_t i = 0; i < nq; ++i) std::memcpy(&qp[i * ix.dstride], q + i * ix.dim, 4ull * ix.dim);
+    float* d_q = nullptr;
+    uint32_t* d_ids = nullptr;
+    float* d_sq = nullptr;
+    float* s_sq = nullptr;
+    const size_t se = pagdev::gt_scratch_elems(ix.n, static_cast<uint32_t>(nq), kk);
+    struct F {
+        void* p[5];
+        ~F() {
+            for (void* x : p) dev_free(x);
+        }
+    } fr{{nullptr, nullptr, nullptr, nullptr, nullptr}};
+    dev_alloc(&d_q, 4 * qp.size());
+    fr.p[0] = d_q;
+    dev_alloc(&d_ids, 4ull * nq * kk);
+    fr.p[1] = d_ids;
+    dev_alloc(&d_sq, 4ull * nq * kk);
+    fr.p[2] = d_sq;
+    dev_alloc(&s_sq, 4 * se);
+    fr.p[3] = s_sq;
+    cuda_check(cudaMemcpyAsync(d_q, qp.data(), 4 * qp.size(), cudaMemcpyHostToDevice, r.stream), "H2D");
+    pagdev::GtLaunch g{};
+    g.base = r.rows;
+    g.n = ix.n;
+    g.padded = ix.padded;
+    g.dstride = ix.dstride;
+    g.queries = d_q;
+    g.nq = static_cast<uint32_t>(nq);
+    g.k = kk;
+    g.out_ids = d_ids;
+    g.out_sq = d_sq;
+    g.scratch_sq = s_sq;
+    g.scratch_id = nullptr;
+    cuda_check(pagdev::launch_ground_truth(g, r.stream), "ground truth kernels");
+    std::vector<uint32_t> hi(nq * kk);
+    std::vector<float> hs(nq * kk);
+    cuda_check(cudaMemcpyAsync(hi.data(), d_ids, 4 * hi.size(), cudaMemcpyDeviceToHost, r.stream), "D2H");
+    cuda_check(cudaMemcpyAsync(hs.data(), d_sq, 4 * hs.size(), cudaMemcpyDeviceToHost, r.stream), "D2H");
+    cuda_check(cudaStreamSynchronize(r.stream), "ground truth");
+    for (uint64_t i = 0; i < nq; ++i) {
+        std::memcpy(ids + i * k, &hi[i * kk], 4ull * kk);
+        std::memcpy(sq + i * k, &hs[i * kk], 4ull * kk);
+    }
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return PAG_GPU_OK;
+    } catch (const PagError& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "out of host memory";
+        return PAG_GPU_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return PAG_GPU_ERUNTIME;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+void pag_gpu_default_params(pag_search_params* p) {
+    p->K = 10;
+    p->efS = 100;
+    p->b_override = 0;
+    p->use_prt = 1;
+    p->use_tfb = 1;
+    p->exact_dist = 1;
+    p->reserved = 0;
+}
+
+int pag_gpu_open(const char* index_path, uint32_t device_mask, pag_gpu_index** out) {
+    return guarded([&] {
+        if (!out || !index_path) throw_err(PAG_GPU_EINVAL, "null argument");
+        *out = nullptr;
+        auto ix = open_index(index_path, device_mask);
+        *out = ix.release();
+    });
+}
+
+int pag_gpu_close(pag_gpu_index* ix) {
+    return guarded([&] {
+        if (!ix) return;
+        for (auto& r : ix->reps) free_replica(r);
+        delete ix;
+    });
+}
+
+int pag_gpu_info(const pag_gpu_index* ix, uint64_t* info, size_t n_info) {
+    return guarded([&] {
+        if (!ix || !info) throw_err(PAG_GPU_EINVAL, "null argument");
+        const uint64_t v[12] = {ix->n, ix->dim, ix->padded, ix->L, ix->m, ix->M, ix->metric,
+                                ix->entries.size(), ix->seed, ix->total_edges, ix->reps.size(),
+                                ix->reps.empty() ? 0 : ix->reps[0].bytes};
+        for (size_t i = 0; i < n_info && i < 12; ++i) info[i] = v[i];
+    });
+}
+
+int pag_gpu_search(pag_gpu_index* ix, const float* q, uint64_t nq, const pag_search_params* params,
+                   uint32_t* ids, float* sq, uint32_t* n_out, pag_search_stats* stats) {
+    return guarded([&] {
+        if (!ix || !params) throw_err(PAG_GPU_EINVAL, "null argument");
+        std::lock_guard<std::mutex> g(ix->mu);
+        const pag_search_params p = *params;
+        validate_params(*ix, p);
+        if (nq == 0) return;
+        if (!q || !n_out || (p.K && (!ids || !sq))) throw_err(PAG_GPU_EINVAL, "null argument");
+        const size_t nd = ix->reps.size();
+        std::vector<uint32_t> status(nd, 0);
+        std::vector<PagError> errs;
+        std::mutex emu;
+        auto shard = [&](size_t d) {
+            const uint64_t q0 = nq * d / nd, q1 = nq * (d + 1) / nd;
+            try {
+                search_on_replica(*ix, ix->reps[d], p, q + q0 * ix->dim, q1 - q0, ids + q0 * p.K,
+                                  sq + q0 * p.K, n_out + q0, stats ? stats + q0 : nullptr, &status[d]);
+            } catch (const PagError& e) {
+                std::lock_guard<std::mutex> lk(emu);
+                errs.push_back(e);
+            }
+        };
+        if (nd == 1) {
+            shard(0);
+        } else {
+            std::vector<std::thread> th;
+            for (size_t d = 0; d < nd; ++d) th.emplace_back(shard, d);
+            for (auto& t : th) t.join();
+        }
+        if (!errs.empty()) throw errs.front();
+        uint32_t so = 0;
+        for (auto s : status) so |= s;
+        if (so & pagdev::kStatusZeroCosineQuery)
+            throw_err(PAG_GPU_EINVAL, "zero query under cosine metric");
+        if (so & pagdev::kStatusVisitedOverflow)
+            throw_err(PAG_GPU_ERUNTIME, "visited set overflow after retries");
+    });
+}
+
+int pag_gpu_search_device(pag_gpu_index* ix, const float* q_dev, uint64_t nq,
+                          const pag_search_params* params, uint32_t* ids_dev, float* sq_dev,
+                          uint32_t* n_out_dev, uint32_t* stats_dev, void* stream) {
+    return guarded([&] {
+        if (!ix || !params) throw_err(PAG_GPU_EINVAL, "null argument");
+        std::lock_guard<std::mutex> g(ix->mu);
+        const pag_search_params p = *params;
+        validate_params(*ix, p);
+        Replica& r = ix->reps[0];
+        cuda_check(cudaSetDevice(r.device), "cudaSetDevice");
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : r.stream;
+        if (nq >= 0xFFFFFFFFull) throw_err(PAG_GPU_EINVAL, "batch too large");
+        run_search(*ix, r, p, q_dev, static_cast<uint32_t>(nq), nullptr, ids_dev, sq_dev, n_out_dev,
+                   stats_dev, s, 0);
+    });
+}
+
+int pag_gpu_ground_truth(pag_gpu_index* ix, const float* queries, uint64_t nq, uint32_t k,
+                         uint32_t* ids, float* sq) {
+    return guarded([&] {
+        if (!ix) throw_err(PAG_GPU_EINVAL, "null argument");
+        std::lock_guard<std::mutex> g(ix->mu);
+        if (nq == 0 || k == 0) return;
+        if (!queries || !ids || !sq) throw_err(PAG_GPU_EINVAL, "null argument");
+        const size_t nd = ix->reps.size();
+        std::vector<PagError> errs;
+        std::mutex emu;
+        auto shard = [&](size_t d) {
+            const uint64_t q0 = nq * d / nd, q1 = nq * (d + 1) / nd;
+            try {
+                ground_truth_on_replica(*ix, ix->reps[d], queries + q0 * ix->dim, q1 - q0, k,
+                                        ids + q0 * k, sq + q0 * k);
+            } catch (const PagError& e) {
+                std::lock_guard<std::mutex> lk(emu);
+                errs.push_back(e);
+            }
+        };
+        if (nd == 1) {
+            shard(0);
+        } else {
+            std::vector<std::thread> th;
+            for (size_t d = 0; d < nd; ++d) th.emplace_back(shard, d);
+            for (auto& t : th) t.join();
+        }
+        if (!errs.empty()) throw errs.front();
+    });
+}
+
+const char* pag_gpu_last_error(void) { return g_err.c_str(); }
+
+const char* pag_gpu_version(void) { return "pag_gpu 0.1 (sm_100a)"; }
+
+}  // extern "C"

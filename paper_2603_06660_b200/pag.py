@@ -1,0 +1,217 @@
+"""Host-side mirror of the reference's search API over the B200 library.
+
+Names, argument meaning and error behaviour follow the reference:
+  SearchParams / SearchStats   proj/include/pag/routing.hpp:13-34
+  SearchResult                 proj/include/pag/routing.hpp:173-177
+  load_index                   proj/include/pag/builder.hpp:157
+  search                       proj/include/pag/routing.hpp:181-188
+  ground_truth / recall_at_k   proj/include/pag/bench.hpp:19-24
+Reference exceptions map to Python ones: std::invalid_argument -> ValueError,
+std::runtime_error -> RuntimeError (same message texts).
+
+The compute path is libpag_gpu.so only (see _lib.py); nothing here computes
+search results on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from ._lib import SearchParamsC, SearchStatsC, check, lib
+
+Candidate = Tuple[int, float]  # (id, squared distance), builder.hpp:18-21
+
+
+@dataclass
+class SearchParams:
+    """routing.hpp:13-22 (collect_pes is build-only and absent)."""
+    K: int = 10
+    efS: int = 100
+    b_override: int = 0
+    use_prt: bool = True
+    use_tfb: bool = True
+    exact_dist: bool = True  # reference-order fp32 distances (bit-identical results)
+
+    def b(self) -> int:
+        return self.b_override if self.b_override else max(10, self.K)
+
+    def to_c(self) -> SearchParamsC:
+        p = SearchParamsC()
+        p.K, p.efS, p.b_override = int(self.K), int(self.efS), int(self.b_override)
+        p.use_prt, p.use_tfb, p.exact_dist = int(self.use_prt), int(self.use_tfb), int(self.exact_dist)
+        return p
+
+
+@dataclass
+class SearchStats:
+    """routing.hpp:24-34, plus edges_scanned (sum of deg over expansions)."""
+    exact_dist_count: int = 0
+    test_count: int = 0
+    pass_count: int = 0
+    visited_count: int = 0
+    edges_scanned: int = 0
+
+    def gamma(self) -> float:
+        return self.pass_count / self.test_count if self.test_count else 0.0
+
+
+@dataclass
+class SearchResult:
+    """routing.hpp:173-177: K nearest (squared distances, ascending)."""
+    results: List[Candidate] = field(default_factory=list)
+    stats: SearchStats = field(default_factory=SearchStats)
+
+
+@dataclass
+class BatchResult:
+    ids: np.ndarray      # nq x K uint32 (first n_out[i] valid)
+    sq: np.ndarray       # nq x K float32
+    n_out: np.ndarray    # nq uint32
+    stats: np.ndarray    # nq x 5 uint64 {exact, test, pass, visited, edges_scanned}
+
+    def result(self, i: int) -> SearchResult:
+        k = int(self.n_out[i])
+        s = self.stats[i]
+        return SearchResult([(int(a), float(b)) for a, b in zip(self.ids[i, :k], self.sq[i, :k])],
+                            SearchStats(*(int(x) for x in s)))
+
+
+class PagIndex:
+    """A PAGIDX01 index resident in HBM on one or more GPUs (move-only in the
+    reference, builder.hpp:62-69; here a handle released by close())."""
+
+    def __init__(self, path: str, devices: Sequence[int] = (0,)):
+        mask = 0
+        for d in devices:
+            mask |= 1 << int(d)
+        self._h = C.c_void_p()
+        check(lib.pag_gpu_open(path.encode(), mask, C.byref(self._h)))
+        info = np.zeros(12, np.uint64)
+        check(lib.pag_gpu_info(self._h, info, 12))
+        (self.n, self.dim, self.padded_dim, self.L, self.m, self.M, metric, self.n_entries,
+         self.seed, self.total_edges, self.n_devices, self.device_bytes) = (int(x) for x in info)
+        self.metric = "cosine" if metric == 1 else "euclidean"
+        self.path = path
+
+    # reference accessors (builder.hpp:71-91)
+    def size(self) -> int:
+        return self.n
+
+    def max_degree(self) -> int:
+        return 2 * self.M
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            check(lib.pag_gpu_close(self._h))
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def search_batch(self, queries: np.ndarray, params: SearchParams) -> BatchResult:
+        q = np.ascontiguousarray(queries, np.float32)
+        if q.ndim == 1:
+            q = q.reshape(1, -1)
+        if q.shape[1] != self.dim:
+            raise ValueError("query dimension mismatch")  # routing.cpp:252
+        nq = q.shape[0]
+        K = int(params.K)
+        ids = np.zeros((nq, K), np.uint32)
+        sq = np.zeros((nq, K), np.float32)
+        n_out = np.zeros(nq, np.uint32)
+        st = (SearchStatsC * max(nq, 1))()
+        pc = params.to_c()
+        check(lib.pag_gpu_search(self._h, q.ctypes.data if nq else None, nq, C.byref(pc),
+                                 ids.ctypes.data if K and nq else None,
+                                 sq.ctypes.data if K and nq else None,
+                                 n_out.ctypes.data if nq else None, st))
+        stats = np.ctypeslib.as_array(C.cast(st, C.POINTER(C.c_uint64)), (max(nq, 1), 5))[:nq].copy()
+        return BatchResult(ids, sq, n_out, stats)
+
+    def search_device(self, q_ptr: int, nq: int, params: SearchParams, ids_ptr: int, sq_ptr: int,
+                      n_out_ptr: int, stats_ptr: int, stream: int = 0) -> None:
+        """Device-resident batch (pointers on the handle's first GPU); async
+        on `stream`. Raw counters: nq x 8 uint32."""
+        pc = params.to_c()
+        check(lib.pag_gpu_search_device(self._h, q_ptr, nq, C.byref(pc), ids_ptr, sq_ptr,
+                                        n_out_ptr, stats_ptr, stream or None))
+
+    def ground_truth(self, queries: np.ndarray, k: int) -> Tuple[np.ndarray, np.ndarray]:
+        """bench.cpp:18-53 over the resident base rows: top-min(k, n) by (sq, id)."""
+        q = np.ascontiguousarray(queries, np.float32).reshape(-1, self.dim)
+        nq = q.shape[0]
+        ids = np.zeros((nq, k), np.uint32)
+        sq = np.zeros((nq, k), np.float32)
+        check(lib.pag_gpu_ground_truth(self._h, q.reshape(-1), nq, k, ids.reshape(-1), sq.reshape(-1)))
+        kk = min(k, self.n)
+        return ids[:, :kk], sq[:, :kk]
+
+
+def load_index(path: str, devices: Sequence[int] = (0,)) -> PagIndex:
+    """builder.hpp:157 load_index, onto the GPUs in `devices`."""
+    return PagIndex(path, devices)
+
+
+def search(index: PagIndex, q, params: Optional[SearchParams] = None) -> SearchResult:
+    """routing.hpp:181-188: one query (dim() raw components)."""
+    params = params or SearchParams()
+    q = np.ascontiguousarray(q, np.float32).reshape(-1)
+    if q.size != index.dim:
+        raise ValueError("query dimension mismatch")
+    return index.search_batch(q.reshape(1, -1), params).result(0)
+
+
+def ground_truth(index: PagIndex, queries: np.ndarray, k_star: int):
+    return index.ground_truth(queries, k_star)
+
+
+def recall_at_k(result_ids, truth_ids, truth_sq, K: int) -> float:
+    """bench.cpp:55-71: |result[0..K) ∩ truth| / K, ids distance-tied with
+    the K-th true neighbour count as hits."""
+    truth_ids = np.asarray(truth_ids)
+    truth_sq = np.asarray(truth_sq, np.float32)
+    k = min(K, len(truth_ids))
+    if k == 0:
+        return 0.0
+    tie = truth_sq[k - 1]
+    first = {}
+    for i, t in enumerate(truth_ids.tolist()):
+        first.setdefault(t, truth_sq[i])
+    hits = 0
+    for r in list(result_ids)[:K]:
+        s = first.get(int(r))
+        if s is not None and s <= tie:
+            hits += 1
+    return hits / K
+
+
+def mean_recall(ids: np.ndarray, n_out: np.ndarray, truth_ids: np.ndarray, truth_sq: np.ndarray,
+                K: int) -> float:
+    """Vectorised recall_at_k averaged over a batch (same tie policy)."""
+    nq = ids.shape[0]
+    k = min(K, truth_ids.shape[1])
+    if k == 0 or nq == 0:
+        return 0.0
+    tie = truth_sq[:, k - 1:k]
+    ok = truth_sq <= tie                                   # nq x kt
+    res = ids[:, :K].astype(np.int64)
+    valid = np.arange(res.shape[1])[None, :] < n_out[:, None]
+    res = np.where(valid, res, -1)
+    hit = (res[:, :, None] == truth_ids[:, None, :].astype(np.int64)) & ok[:, None, :]
+    return float(hit.any(axis=2).sum(axis=1).mean() / K)
