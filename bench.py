@@ -1,0 +1,453 @@
+#!/usr/bin/env python
+"""Benchmark: batched PAG search QPS at recall@K = 0.95 on B200.
+
+Workload (BASELINE.json configs[1], the north-star config): n = 1,000,000
+base vectors, d = 768, unit-normalised 4,096-centre Gaussian mixture
+(sigma 0.4), 10,000 queries from the same mixture, L2 metric, K = 10, index
+built by the reference CPU build with its default parameters. Synthetic,
+seeded data stands in for the paper's datasets.
+
+A "step" is one pass of the search over the whole 10,000-query batch.
+  value : QPS with the queries already in HBM (device-timed, CUDA events on
+          the launching stream), at the smallest swept efS whose recall@K
+          against exact ground truth (GPU, reference-order fp32) is >= 0.95.
+  e2e   : the same batch through the C ABI pag_gpu_search with host buffers
+          (pinned queries; H2D + kernel + D2H + sync inside the timed region).
+  roofline : algorithmic bytes per query (SURVEY.md §8(d) B_q, from the
+          kernel's own counters) / kernel time, against MEASURED_PEAKS.json.
+  cpu_baseline : the unmodified reference search (oracle/_ref/pag_ref,
+          compiled from the reference's sources) on this host's cores.
+
+Multi-GPU (torchrun): every rank holds a full index replica and searches its
+own 10,000-query batch (weak scaling, no collective on the data path); the
+step time is the max over ranks.
+
+--impl reference: the reference's own CPU search (oracle/_ref/pag_ref) with
+all host threads on the same index/queries/efS; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import shutil
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2603_06660_b200.fvecs import CONFIGS, gaussian_mixture, read_fvecs, write_fvecs  # noqa: E402
+
+REF_BIN = os.path.join(ROOT, "oracle", "_ref", "pag_ref")
+SEEDS = dict(centre=7, base=1, query=2)
+
+
+def log(*a):
+    print("[bench]", *a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+# data + index (cached by content key; rebuilt when absent)
+# ---------------------------------------------------------------------------
+def cache_paths(cfg_name: str, cache_dir: str):
+    cfg = CONFIGS[cfg_name]
+    key = hashlib.sha1(json.dumps([cfg_name, cfg["n"], cfg["d"], cfg["centres"], cfg["sigma"],
+                                   cfg["unit"], cfg["nq"], SEEDS, "ref-default-build-v1"]).encode()).hexdigest()[:12]
+    d = os.path.join(cache_dir, f"{cfg_name}-{key}")
+    return d, dict(base=os.path.join(d, "base.fvecs"), queries=os.path.join(d, "queries.fvecs"),
+                   index=os.path.join(d, "index.pagidx"), gt=os.path.join(d, "gt.npz"),
+                   build=os.path.join(d, "build.json"))
+
+
+def prepare(cfg_name: str, cache_dir: str, threads: int):
+    cfg = CONFIGS[cfg_name]
+    d, p = cache_paths(cfg_name, cache_dir)
+    os.makedirs(d, exist_ok=True)
+    if not os.path.exists(p["queries"]):
+        t = time.time()
+        q = gaussian_mixture(cfg["nq"], cfg["d"], cfg["centres"], cfg["sigma"], seed=SEEDS["query"],
+                             centre_seed=SEEDS["centre"], unit=cfg["unit"])
+        write_fvecs(p["queries"], q)
+        log(f"queries generated in {time.time() - t:.1f}s")
+    if not os.path.exists(p["index"]):
+        if not os.path.exists(p["base"]):
+            t = time.time()
+            x = gaussian_mixture(cfg["n"], cfg["d"], cfg["centres"], cfg["sigma"], seed=SEEDS["base"],
+                                 centre_seed=SEEDS["centre"], unit=cfg["unit"])
+            write_fvecs(p["base"], x)
+            del x
+            log(f"base generated in {time.time() - t:.1f}s")
+        if not os.path.exists(REF_BIN):
+            raise RuntimeError("oracle/_ref/pag_ref missing (build it where /root/reference exists)")
+        t = time.time()
+        tmp = p["index"] + ".tmp"
+        out = subprocess.run([REF_BIN, "build", f"--data={p['base']}", f"--out={tmp}",
+                              f"--threads={threads}"], check=True, capture_output=True, text=True)
+        os.replace(tmp, p["index"])
+        with open(p["build"], "w") as f:
+            f.write(out.stdout)
+        log(f"reference build ({threads} threads) in {time.time() - t:.1f}s: {out.stdout.strip()}")
+        os.remove(p["base"])  # the index file carries the rows
+    return cfg, p
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        if shutil.which("nvidia-smi") is None:
+            return self
+        self.path = f"/tmp/pag_clocks_{os.getpid()}.csv"
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,utilization.gpu")
+        self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits", "-lms", "100"],
+                                     stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.path or not os.path.exists(self.path):
+            return None
+        rows = []
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[2:6], float(parts[6])))
+            except ValueError:
+                continue
+        os.remove(self.path)
+        if not rows:
+            return None
+        loaded = [r for r in rows if r[3] > 0] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in loaded for i, v in enumerate(r[2]) if v.lower() == "active"})
+        return {"sm_mhz": float(np.median([r[0] for r in loaded])), "sm_max_mhz": loaded[0][1],
+                "reasons": reasons, "samples": len(loaded)}
+
+
+# ---------------------------------------------------------------------------
+def algorithmic_bytes(stats: np.ndarray, dpad: int, L: int, K: int) -> float:
+    """B_q = 4 d + sum_exp (4 + deg (16 + ceil(L/2))) + exact 4 d + 8 K."""
+    exact, visited, edges = stats[:, 0].astype(np.float64), stats[:, 3].astype(np.float64), stats[:, 4].astype(np.float64)
+    cb = (L + 1) // 2
+    bq = 4.0 * dpad + 4.0 * visited + edges * (16 + cb) + exact * 4.0 * dpad + 8.0 * K
+    return float(bq.sum())
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def cpu_reference(index_path: str, queries_path: str, K: int, efS: int, threads: int, limit: int, reps: int):
+    out = subprocess.run([REF_BIN, "search", f"--index={index_path}", f"--queries={queries_path}",
+                          f"--K={K}", f"--efS={efS}", f"--threads={threads}", f"--limit={limit}",
+                          f"--reps={reps}"], check=True, capture_output=True, text=True)
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="pag", choices=["pag", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--efs", type=int, default=0, help="fixed efS (default: sweep to recall 0.95)")
+    ap.add_argument("--target-recall", type=float, default=0.95)
+    ap.add_argument("--cache-dir", default=os.environ.get("PAG_CACHE", "/tmp/pag_b200_cache"))
+    ap.add_argument("--fast-dist", action="store_true", help="warp-tree distances instead of reference order")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    threads = os.cpu_count() or 1
+
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "gloo" if args.impl == "reference" else "nccl"
+        if backend == "nccl":
+            torch.cuda.set_device(local_rank)
+        dist.init_process_group(backend=backend)
+
+    # data + index: rank 0 prepares, the others wait
+    if rank == 0:
+        cfg, paths = prepare(args.config, args.cache_dir, threads)
+    if dist is not None:
+        dist.barrier()
+    if rank != 0:
+        cfg, paths = prepare(args.config, args.cache_dir, threads)
+    K = cfg["K"]
+
+    if args.impl == "reference":
+        run_reference(args, cfg, paths, rank, world, threads, dist)
+        return
+    run_pag(args, cfg, paths, rank, world, local_rank, threads, dist)
+
+
+def choose_efs(ix, queries, gt_ids, gt_sq, cfg, args, pag):
+    K = cfg["K"]
+    sweep = []
+    chosen = None
+    for efs in cfg["efs"]:
+        if efs < K:
+            continue
+        r = ix.search_batch(queries, pag.SearchParams(K=K, efS=efs, exact_dist=not args.fast_dist))
+        rec = pag.mean_recall(r.ids, r.n_out, gt_ids, gt_sq, K)
+        st = r.stats.astype(np.float64)
+        sweep.append({"efS": efs, "recall": round(rec, 4), "exact": round(float(st[:, 0].mean()), 1),
+                      "tests": round(float(st[:, 1].mean()), 1), "passes": round(float(st[:, 2].mean()), 1),
+                      "expansions": round(float(st[:, 3].mean()), 1)})
+        log(f"sweep efS={efs} recall@{K}={rec:.4f} exact={st[:, 0].mean():.1f} exp={st[:, 3].mean():.1f}")
+        if rec >= args.target_recall and chosen is None:
+            chosen = efs
+            break
+    if chosen is None:
+        chosen = sweep[-1]["efS"]
+    return chosen, sweep
+
+
+def run_pag(args, cfg, paths, rank, world, local_rank, threads, dist):
+    import torch
+
+    import paper_2603_06660_b200 as pag
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    K = cfg["K"]
+    t0 = time.time()
+    ix = pag.load_index(paths["index"], devices=(local_rank,))
+    log(f"rank {rank}: index resident on cuda:{local_rank} in {time.time() - t0:.1f}s "
+        f"({ix.device_bytes / 2**30:.2f} GiB, {ix.total_edges} edges)")
+    queries = read_fvecs(paths["queries"])
+    nq = queries.shape[0]
+
+    # ground truth (exact, GPU) + operating point, on rank 0
+    efs, sweep, gt_s = args.efs, [], None
+    if rank == 0:
+        if os.path.exists(paths["gt"]):
+            z = np.load(paths["gt"])
+            gt_ids, gt_sq = z["ids"], z["sq"]
+        else:
+            t = time.time()
+            gt_ids, gt_sq = ix.ground_truth(queries, K)
+            gt_s = time.time() - t
+            np.savez(paths["gt"], ids=gt_ids, sq=gt_sq)
+            log(f"ground truth ({nq} x {ix.n}) on GPU in {gt_s:.1f}s")
+        if not efs:
+            efs, sweep = choose_efs(ix, queries, gt_ids, gt_sq, cfg, args, pag)
+            with open(os.path.join(os.path.dirname(paths["index"]), "operating_point.json"), "w") as f:
+                json.dump({"efS": efs, "sweep": sweep}, f)
+        r = ix.search_batch(queries, pag.SearchParams(K=K, efS=efs, exact_dist=not args.fast_dist))
+        recall = pag.mean_recall(r.ids, r.n_out, gt_ids, gt_sq, K)
+    if dist is not None:
+        t = torch.tensor([efs], dtype=torch.int64, device=dev)
+        dist.broadcast(t, 0)
+        efs = int(t.item())
+    params = pag.SearchParams(K=K, efS=efs, exact_dist=not args.fast_dist)
+
+    # device-resident batch
+    q_dev = torch.from_numpy(queries).to(dev)
+    ids_dev = torch.empty((nq, K), dtype=torch.int32, device=dev)
+    sq_dev = torch.empty((nq, K), dtype=torch.float32, device=dev)
+    n_dev = torch.empty((nq,), dtype=torch.int32, device=dev)
+    st_dev = torch.empty((nq, 8), dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        ix.search_device(q_dev.data_ptr(), nq, params, ids_dev.data_ptr(), sq_dev.data_ptr(),
+                         n_dev.data_ptr(), st_dev.data_ptr(), stream.cuda_stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize(dev)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with Clocks(local_rank) as clk:
+        ev[0].record(stream)
+        for i in range(args.steps):
+            step()
+            ev[i + 1].record(stream)
+        torch.cuda.synchronize(dev)
+    per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    if dist is not None:
+        dist.barrier()
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * nq * args.steps / (total_ms / 1e3)
+
+    stats = st_dev.cpu().numpy().view(np.uint32).astype(np.uint64)
+    status = int(np.bitwise_or.reduce(stats[:, 5])) if nq else 0
+    bytes_total = algorithmic_bytes(stats[:, [0, 1, 2, 3, 4]], ix.padded_dim, ix.L, K)
+    kernel_ms = float(np.mean(per_step))
+    achieved = bytes_total / (kernel_ms / 1e3) / 1e9
+    peak, peak_kind = load_peaks()
+
+    # e2e through the C ABI with host buffers (pinned queries)
+    q_pin = torch.empty((nq, queries.shape[1]), dtype=torch.float32, pin_memory=True)
+    q_pin.numpy()[:] = queries
+    qh = q_pin.numpy()
+    for _ in range(2):
+        ix.search_batch(qh, params)
+    torch.cuda.synchronize(dev)
+    e2e_steps = max(3, min(args.steps, 10))
+    if dist is not None:
+        dist.barrier()
+    t = time.perf_counter()
+    for _ in range(e2e_steps):
+        res = ix.search_batch(qh, params)
+    e2e_s = time.perf_counter() - t
+    if dist is not None:
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e_qps = world * nq * e2e_steps / e2e_s
+    h2d = nq * queries.shape[1] * 4
+    d2h = nq * K * 8 + nq * 4 + nq * 8 * 4
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    # cpu baseline (reference search, all host cores, bounded sample)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline and os.path.exists(REF_BIN):
+        lim = min(nq, 4000)
+        c = cpu_reference(paths["index"], paths["queries"], K, efs, threads, lim, 3)
+        cpu = {"value": round(c["qps"], 1), "unit": "queries/s", "cores": threads, "kind": "reference",
+               "sample": f"first {lim} queries x 3 timed sweeps after 1 warm sweep, "
+                         f"reference search (oracle/_ref/pag_ref, g++ -O3), {threads} threads on {cpu_model()}"}
+    sm = stats.astype(np.float64)
+    line = {
+        "metric": f"QPS at recall@{K}={args.target_recall} (batched search, {cfg['n']}x{cfg['d']})",
+        "value": round(value, 1),
+        "unit": "queries/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(3, args.warmup),
+        "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (seeded Gaussian mixture per BASELINE.json; index from the reference CPU build)",
+        "config": {"workload": args.config, "n": cfg["n"], "d": cfg["d"], "queries_per_step": nq,
+                   "K": K, "efS": efs, "recall": round(recall, 4), "sweep": sweep,
+                   "distance_mode": "warp-tree" if args.fast_dist else "reference-order (bit-exact)",
+                   "l2": "index (>3 GB) exceeds the 126 MB L2; no flush needed",
+                   "parallelism": f"query shards, index replica per GPU x{world}"},
+        "e2e": {"value": round(e2e_qps, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": args.steps,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind,
+                     "bytes_per_query": round(bytes_total / nq, 1)},
+        "per_query": {"exact": round(float(sm[:, 0].mean()), 2), "tests": round(float(sm[:, 1].mean()), 2),
+                      "passes": round(float(sm[:, 2].mean()), 2), "expansions": round(float(sm[:, 3].mean()), 2),
+                      "edges_scanned": round(float(sm[:, 4].mean()), 2)},
+        "status_bits": status,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def run_reference(args, cfg, paths, rank, world, threads, dist):
+    K = cfg["K"]
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    efs = args.efs or default_efs(cfg, paths)
+    lim = min(cfg["nq"], 4000)
+    vals = []
+    c = cpu_reference(paths["index"], paths["queries"], K, efs, threads, lim, max(1, args.steps))
+    vals.append(c["qps"])
+    line = {
+        "impl": "reference",
+        "metric": f"QPS at recall@{K}={args.target_recall} (batched search, {cfg['n']}x{cfg['d']})",
+        "value": round(c["qps"], 1),
+        "unit": "queries/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": 1,
+        "ms_per_step": round(1e3 * c["seconds_mean"], 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (seeded Gaussian mixture per BASELINE.json; index from the reference CPU build)",
+        "config": {"workload": args.config, "n": cfg["n"], "d": cfg["d"], "queries_per_step": lim,
+                   "K": K, "efS": efs, "parallelism": f"{threads} host threads"},
+        "e2e": {"value": round(c["qps"], 1), "unit": "queries/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": round(c["qps"], 1), "unit": "queries/s", "cores": threads,
+                         "kind": "reference",
+                         "sample": f"first {lim} queries per step, 1 warm sweep, reference search "
+                                   f"(oracle/_ref/pag_ref) on {cpu_model()}"},
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def default_efs(cfg, paths):
+    """The operating point the GPU arm found (cached next to the index), else
+    the survey's efS for recall 0.95 on this config."""
+    op = os.path.join(os.path.dirname(paths["index"]), "operating_point.json")
+    if os.path.exists(op):
+        return int(json.load(open(op))["efS"])
+    return {"cfg1": 30, "cfg2": 80, "cfg3": 100, "cfg4": 4000}[next(k for k, v in CONFIGS.items() if v is cfg)]
+
+
+if __name__ == "__main__":
+    main()

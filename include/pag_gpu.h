@@ -113,6 +113,23 @@ int pag_gpu_search_device(pag_gpu_index* ix, const float* q_dev, uint64_t nq,
 int pag_gpu_ground_truth(pag_gpu_index* ix, const float* queries, uint64_t nq, uint32_t k,
                          uint32_t* ids, float* sq);
 
+/* Host-only: parse and validate a PAGIDX01 file exactly as pag_gpu_open
+ * does (same errors), without touching a GPU; fills info[0..9] as
+ * pag_gpu_info (n_devices and device bytes are 0). */
+int pag_gpu_inspect(const char* index_path, uint64_t* info, size_t n_info);
+
+/* Host-only: the regenerated reference family the loader uploads.
+ * Replaces: ReferenceSet build_reference_set(uint32_t padded_dim, uint32_t L,
+ *           uint32_t m, uint64_t seed), proj/include/pag/projection.hpp:35,
+ *           proj/src/projection.cpp:40-74 (same validation messages).
+ * out: L*m*(padded_dim/L) floats, refs[(l*m + j)*sub_dim + c]. */
+int pag_gpu_reference_family(uint32_t padded_dim, uint32_t L, uint32_t m, uint64_t seed,
+                             float* out, size_t n_out);
+
+/* Replaces: uint32_t default_subspace_count(uint32_t dim),
+ *           proj/include/pag/projection.hpp:83, proj/src/projection.cpp:151-166. */
+uint32_t pag_gpu_default_subspace_count(uint32_t dim);
+
 /* Thread-local message of the last failing call on this thread. */
 const char* pag_gpu_last_error(void);
 

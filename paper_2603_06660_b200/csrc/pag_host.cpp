@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -257,7 +258,8 @@ void free_replica(Replica& r) {
 // ---------------------------------------------------------------------------
 // PAGIDX01 v1 ingest (builder.cpp:434-492) straight into the device layout
 // ---------------------------------------------------------------------------
-std::unique_ptr<pag_gpu_index> open_index(const char* path, uint32_t device_mask) {
+// dry = true: parse and validate the whole file on the host only (no GPU).
+std::unique_ptr<pag_gpu_index> open_index(const char* path, uint32_t device_mask, bool dry = false) {
     Mapped mp;
     mp.fd = ::open(path, O_RDONLY);
     if (mp.fd < 0) throw_err(PAG_GPU_ERUNTIME, std::string("cannot open index: ") + path);
@@ -306,14 +308,16 @@ std::unique_ptr<pag_gpu_index> open_index(const char* path, uint32_t device_mask
     ix->block_bytes = ix->slot_stride * (16u + 4u * ix->cwp);
 
     std::vector<int> devs;
-    if (device_mask == 0) device_mask = 1;
-    int ndev = 0;
-    cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
-    for (int d = 0; d < 32; ++d)
-        if (device_mask & (1u << d)) {
-            if (d >= ndev) throw_err(PAG_GPU_EINVAL, "device_mask names a missing GPU");
-            devs.push_back(d);
-        }
+    if (!dry) {
+        if (device_mask == 0) device_mask = 1;
+        int ndev = 0;
+        cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+        for (int d = 0; d < 32; ++d)
+            if (device_mask & (1u << d)) {
+                if (d >= ndev) throw_err(PAG_GPU_EINVAL, "device_mask names a missing GPU");
+                devs.push_back(d);
+            }
+    }
 
     const uint64_t n = ix->n;
     const size_t row_bytes = 4ull * ix->dstride;
@@ -358,20 +362,34 @@ std::unique_ptr<pag_gpu_index> open_index(const char* path, uint32_t device_mask
     const size_t chunk_bytes = CH * ix->block_bytes;
     uint8_t* stage[2] = {nullptr, nullptr};
     uint32_t* dstage[2] = {nullptr, nullptr};
-    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&stage[0]), chunk_bytes, 0), "cudaHostAlloc");
-    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&stage[1]), chunk_bytes, 0), "cudaHostAlloc");
-    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&dstage[0]), CH * 4, 0), "cudaHostAlloc");
-    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&dstage[1]), CH * 4, 0), "cudaHostAlloc");
+    auto host_alloc = [dry](void** p, size_t bytes) {
+        if (dry) {
+            *p = std::malloc(bytes);
+            if (!*p) throw std::bad_alloc();
+        } else {
+            cuda_check(cudaHostAlloc(p, bytes, 0), "cudaHostAlloc");
+        }
+    };
+    host_alloc(reinterpret_cast<void**>(&stage[0]), chunk_bytes);
+    host_alloc(reinterpret_cast<void**>(&stage[1]), chunk_bytes);
+    host_alloc(reinterpret_cast<void**>(&dstage[0]), CH * 4);
+    host_alloc(reinterpret_cast<void**>(&dstage[1]), CH * 4);
     struct Free {
         uint8_t** s;
         uint32_t** d;
+        bool dry;
         ~Free() {
             for (int i = 0; i < 2; ++i) {
-                if (s[i]) cudaFreeHost(s[i]);
-                if (d[i]) cudaFreeHost(d[i]);
+                if (dry) {
+                    std::free(s[i]);
+                    std::free(d[i]);
+                } else {
+                    if (s[i]) cudaFreeHost(s[i]);
+                    if (d[i]) cudaFreeHost(d[i]);
+                }
             }
         }
-    } fr{stage, dstage};
+    } fr{stage, dstage, dry};
     const uint32_t S = ix->slot_stride, cb = ix->cb, cwp = ix->cwp;
     const size_t rec = 4 + cb + 12;
     int buf = 0;
@@ -426,7 +444,9 @@ std::unique_ptr<pag_gpu_index> open_index(const char* path, uint32_t device_mask
             const uint64_t cnt = std::min<uint64_t>(RCH, n - i0);
             for (auto& r : ix->reps) cudaStreamSynchronize(r.stream);
             uint8_t* st = stage[buf];
-            if (ix->dstride == ix->padded) {
+            if (dry) {
+                // host-only inspection: rows are validated for presence only
+            } else if (ix->dstride == ix->padded) {
                 std::memcpy(st, rows + i0 * row_bytes, cnt * row_bytes);
             } else {
                 std::memset(st, 0, cnt * row_bytes);
@@ -524,6 +544,10 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     // per-slot HBM visited table
     uint64_t want = 2ull * (16ull * p.efS + 512ull);
     L.gtab_log2 = std::max<uint32_t>(std::max<uint32_t>(12, ceil_log2(want)), gt_log2_min);
+    if (const char* e = std::getenv("PAG_GPU_GTAB_LOG2")) {  // test hook: force the overflow path
+        const uint32_t forced = static_cast<uint32_t>(std::atoi(e));
+        if (forced >= 4 && forced < 28) L.gtab_log2 = std::max(forced, gt_log2_min);
+    }
     int bps = 0;
     size_t smem = static_cast<size_t>(L.warp_smem_bytes) * kWarpsPerBlock;
     cuda_check(pagdev::search_occupancy(kWarpsPerBlock, smem, &bps), "occupancy");
@@ -536,6 +560,7 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
 void ensure_scratch(Replica& r, Plan& pl) {
     auto& L = pl.L;
     const size_t slots = static_cast<size_t>(pl.grid) * kWarpsPerBlock;
+    if (!std::getenv("PAG_GPU_GTAB_LOG2")) L.gtab_log2 = std::max(L.gtab_log2, r.gtab_log2);  // only grow
     if (slots > r.slots || L.gtab_log2 != r.gtab_log2) {
         const size_t ns = std::max(slots, r.slots);
         dev_free(r.gtab);
@@ -730,6 +755,27 @@ int pag_gpu_open(const char* index_path, uint32_t device_mask, pag_gpu_index** o
         *out = ix.release();
     });
 }
+
+int pag_gpu_inspect(const char* index_path, uint64_t* info, size_t n_info) {
+    return guarded([&] {
+        if (!index_path || !info) throw_err(PAG_GPU_EINVAL, "null argument");
+        auto ix = open_index(index_path, 0, true);
+        const uint64_t v[12] = {ix->n, ix->dim, ix->padded, ix->L, ix->m, ix->M, ix->metric,
+                                ix->entries.size(), ix->seed, ix->total_edges, 0, 0};
+        for (size_t i = 0; i < n_info && i < 12; ++i) info[i] = v[i];
+    });
+}
+
+int pag_gpu_reference_family(uint32_t padded_dim, uint32_t L, uint32_t m, uint64_t seed, float* out,
+                             size_t n_out) {
+    return guarded([&] {
+        auto refs = reference_family(padded_dim, L, m, seed);
+        if (!out || n_out < refs.size()) throw_err(PAG_GPU_EINVAL, "output buffer too small");
+        std::memcpy(out, refs.data(), 4 * refs.size());
+    });
+}
+
+uint32_t pag_gpu_default_subspace_count(uint32_t dim) { return default_L(dim); }
 
 int pag_gpu_close(pag_gpu_index* ix) {
     return guarded([&] {

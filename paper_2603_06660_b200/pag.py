@@ -208,10 +208,15 @@ def mean_recall(ids: np.ndarray, n_out: np.ndarray, truth_ids: np.ndarray, truth
     k = min(K, truth_ids.shape[1])
     if k == 0 or nq == 0:
         return 0.0
-    tie = truth_sq[:, k - 1:k]
-    ok = truth_sq <= tie                                   # nq x kt
-    res = ids[:, :K].astype(np.int64)
-    valid = np.arange(res.shape[1])[None, :] < n_out[:, None]
-    res = np.where(valid, res, -1)
-    hit = (res[:, :, None] == truth_ids[:, None, :].astype(np.int64)) & ok[:, None, :]
-    return float(hit.any(axis=2).sum(axis=1).mean() / K)
+    total = 0.0
+    step = max(1, int(2e7 // max(1, K * truth_ids.shape[1])))
+    for s in range(0, nq, step):
+        e = min(nq, s + step)
+        tie = truth_sq[s:e, k - 1:k]
+        ok = truth_sq[s:e] <= tie                                  # q x kt
+        res = ids[s:e, :K].astype(np.int64)
+        valid = np.arange(res.shape[1])[None, :] < n_out[s:e, None]
+        res = np.where(valid, res, -1)
+        hit = (res[:, :, None] == truth_ids[s:e, None, :].astype(np.int64)) & ok[:, None, :]
+        total += float(hit.any(axis=2).sum())
+    return total / (nq * K)

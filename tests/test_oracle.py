@@ -1,0 +1,256 @@
+"""CPU tests: pin the oracle (oracle/pag_oracle.c) to the reference.
+
+1. Bit-exact agreement with the unmodified reference (oracle/_ref/pag_ref)
+   on indexes the reference built: ids, squared distances, counters,
+   projection tables, the regenerated reference family, ground truth.
+2. The reference's recorded golden values (proj/test_output.txt:8,12) on its
+   acceptance fixture.
+3. The reference unit-test KATs (proj/tests/test_routing.cpp,
+   test_projection.cpp, test_vecstore.cpp, test_bench.cpp), re-expressed.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import assert_same_results
+from oracle import oracle as O
+
+CASES = [
+    ("euc48", 10, 10), ("euc48", 10, 40), ("euc48", 10, 200), ("euc48", 1, 1), ("euc48", 32, 64),
+    ("euc48", 100, 300), ("cos20", 10, 50), ("cos20", 5, 5), ("tail10", 10, 30), ("tail10", 40, 90),
+    ("deg64", 10, 60), ("deg64", 64, 128),
+]
+
+
+@pytest.mark.parametrize("name,K,efS", CASES)
+def test_oracle_matches_reference(built, fixture_dir, name, K, efS):
+    fx = built(name)
+    ix = O.OracleIndex(fx["index"])
+    got = ix.search(fx["queries"], K, efS)
+    ids, sq, n_out, st, _ = O.ref_search(fx["index"], fx["q_path"], K, efS,
+                                         os.path.join(fixture_dir, f"r_{name}_{K}_{efS}.bin"), no_warm=True)
+    assert_same_results((got[0], got[1], got[2], got[3][:, :4]), (ids, sq, n_out, st), f"{name} K={K} efS={efS}")
+
+
+@pytest.mark.parametrize("flags", [dict(use_prt=False), dict(use_tfb=False), dict(b_override=32)])
+def test_oracle_ablations_match_reference(built, fixture_dir, flags):
+    fx = built("euc48")
+    ix = O.OracleIndex(fx["index"])
+    got = ix.search(fx["queries"], 10, 80, **flags)
+    kw = {"no_prt": not flags.get("use_prt", True), "no_tfb": not flags.get("use_tfb", True)}
+    if "b_override" in flags:
+        kw["b"] = flags["b_override"]
+    ids, sq, n_out, st, _ = O.ref_search(fx["index"], fx["q_path"], 10, 80,
+                                         os.path.join(fixture_dir, "abl.bin"), no_warm=True, **kw)
+    assert_same_results((got[0], got[1], got[2], got[3][:, :4]), (ids, sq, n_out, st), str(flags))
+    if not flags.get("use_prt", True):
+        # devolved mode: every candidate edge is a trivially passed test (test_routing.cpp:270)
+        assert np.array_equal(got[3][:, 1], got[3][:, 2])
+
+
+@pytest.mark.parametrize("name", ["euc48", "cos20", "tail10"])
+def test_tables_and_refs_match_reference(built, fixture_dir, name):
+    fx = built(name)
+    ix = O.OracleIndex(fx["index"])
+    refs, entries = O.ref_refs(fx["index"], os.path.join(fixture_dir, f"refs_{name}.bin"))
+    assert np.array_equal(refs.view(np.uint32), ix.refs().view(np.uint32))
+    assert np.array_equal(entries, ix.entry_nodes())
+    tabs = O.ref_tables(fx["index"], fx["q_path"], os.path.join(fixture_dir, f"tab_{name}.bin"))
+    mine = np.stack([ix.query_table(q) for q in fx["queries"]])
+    assert np.array_equal(tabs.view(np.uint32), mine.view(np.uint32))
+
+
+def test_golden_acceptance_values(acceptance, fixture_dir):
+    """proj/test_output.txt:8,12 — recall and gamma on the acceptance fixture,
+    plus the survey-derived mean exact-distance counts and structure."""
+    ix = O.OracleIndex(acceptance["index"])
+    assert ix.total_edges == 209935 and int(ix.entry_nodes()[0]) == 2662 and ix.L == 16
+    gi, gs = O.ground_truth(acceptance["base"], acceptance["queries"], 100)
+    ri, rs = O.ref_gt(acceptance["base_path"], acceptance["q_path"], 100, os.path.join(fixture_dir, "gt.bin"))
+    assert np.array_equal(gi, ri) and np.array_equal(gs.view(np.uint32), rs.view(np.uint32))
+    golden = {(10, 200): (0.9560, 0.2052, 1208.04), (10, 400): (0.9930, 0.2202, 2235.09),
+              (100, 500): (0.9594, 0.2550, 2482.68), (100, 800): (0.9813, 0.2651, 3554.23)}
+    for (K, efS), (rec_w, gam_w, ex_w) in golden.items():
+        ids, sq, n_out, st = ix.search(acceptance["queries"], K, efS)
+        rec = np.mean([O.recall_at_k(ids[i, :n_out[i]], gi[i], gs[i], K) for i in range(len(ids))])
+        gam = np.mean(st[:, 2] / st[:, 1])
+        assert round(rec, 4) == rec_w and round(gam, 4) == gam_w and round(st[:, 0].mean(), 2) == ex_w
+
+
+# ------------------------------------------------------------------ KATs
+def test_prt_clamp_kat():  # test_routing.cpp:60-69
+    L = O.lib()
+    assert not L.pago_prt_test(0.999, 1.0, 1.0 + 2e-6)
+    assert L.pago_prt_test(-0.999, 1.0, -1.0)
+    assert L.pago_prt_test(-0.999, 1.0, -50.0)
+    assert L.pago_prt_test(0.5, 1.0, 0.5)
+    assert not L.pago_prt_test(0.49, 1.0, 0.5)
+    assert L.pago_prt_test(0.45, 0.5, 0.9)
+    assert not L.pago_prt_test(0.44, 0.5, 0.9)
+
+
+def test_prt_threshold_law_of_cosines():  # test_routing.cpp:31-58
+    L = O.lib()
+    rng = np.random.default_rng(101)
+    for _ in range(500):
+        th = rng.uniform(0.02, np.pi - 0.02)
+        eu, dq = rng.uniform(0.1, 5.0, 2)
+        wx, wy = eu * np.cos(th), eu * np.sin(th)
+        wq = np.hypot(wx - dq, wy)
+        assert L.pago_prt_test(np.cos(th), 1.0, L.pago_prt_threshold(eu, dq, wq * 1.01))
+        assert not L.pago_prt_test(np.cos(th), 1.0, L.pago_prt_threshold(eu, dq, wq * 0.99))
+
+
+def test_ring_overwrite_kat():  # test_routing.cpp:86-96
+    out = np.zeros(3, np.uint32)
+    n = O.lib().pago_ring_kat(3, np.arange(5, dtype=np.uint32), np.arange(5, dtype=np.float32), 5, out)
+    assert n == 3 and list(out) == [2, 3, 4]
+
+
+def _dump(st, which, cap=64):
+    ids = np.zeros(cap, np.uint32)
+    sq = np.zeros(cap, np.float32)
+    vis = np.zeros(cap, np.uint8)
+    n = O.lib().pago_tfb_dump(st, which, ids, sq, vis, cap)
+    return ids[:n], sq[:n], vis[:n]
+
+
+def test_admission_and_zmax_kat():  # test_routing.cpp:98-115
+    L = O.lib()
+    st = L.pago_tfb_new(100, 3, 10)
+    assert L.pago_tfb_admission_sq(st) == np.inf
+    L.pago_tfb_seed(st, 0, 9.0)
+    L.pago_tfb_seed(st, 1, 4.0)
+    L.pago_tfb_seed(st, 2, 16.0)
+    assert L.pago_tfb_admission_sq(st) == 16.0
+    assert abs(L.pago_tfb_admission_dist(st) - 4.0) < 1e-6
+    L.pago_tfb_admit(st, 3, 1.0)
+    assert len(_dump(st, 0)[0]) == 3 and L.pago_tfb_admission_sq(st) == 9.0
+    assert list(_dump(st, 2)[0]) == [2]
+    assert L.pago_tfb_validate(st) == 0
+    L.pago_tfb_free(st)
+
+
+def test_end_round_kat():  # test_routing.cpp:117-168
+    L = O.lib()
+    st = L.pago_tfb_new(100, 3, 10)
+    for i, s in ((10, 5.0), (11, 2.0), (12, 7.0)):
+        L.pago_tfb_seed(st, i, s)
+    for i in range(3):
+        L.pago_tfb_set_visited(st, i, 1)
+    L.pago_tfb_push_fp(st, 20, 3.0)
+    L.pago_tfb_push_fp(st, 21, 8.0)
+    L.pago_tfb_push_fp(st, 22, 1.0)
+    L.pago_tfb_admit(st, 13, 0.5)
+    L.pago_tfb_set_visited(st, 2, 1)
+    assert L.pago_tfb_end_round(st) == 1 and L.pago_tfb_validate(st) == 0
+    ids, sq, vis = _dump(st, 0)
+    assert sorted(zip(sq.tolist(), ids.tolist())) == [(1.0, 22), (3.0, 20), (7.0, 12)]
+    assert not vis.any()
+    assert list(_dump(st, 2)[0]) == [21]
+    assert {10, 11, 13} <= set(_dump(st, 3)[0].tolist())
+    L.pago_tfb_free(st)
+    st = L.pago_tfb_new(10, 2, 5)
+    L.pago_tfb_seed(st, 0, 1.0)
+    L.pago_tfb_set_visited(st, 0, 1)
+    assert L.pago_tfb_end_round(st) == 0
+    L.pago_tfb_free(st)
+
+
+def test_bounded_result_list_kat():  # test_routing.cpp:170-182
+    L = O.lib()
+    st = L.pago_tfb_new(10, 2, 3)
+    for i, s in ((5, 9.0), (1, 1.0), (2, 4.0), (3, 2.0)):
+        L.pago_tfb_push_result(st, i, s)
+    assert list(_dump(st, 3)[0]) == [1, 3, 2]
+    assert L.pago_tfb_validate(st) == 0
+    L.pago_tfb_free(st)
+
+
+def test_code_packing_kat():  # test_projection.cpp:40-54
+    L = O.lib()
+    buf = np.zeros(8, np.uint8)
+    want = np.random.default_rng(5).integers(0, 16, 16)
+    for l in range(16):
+        L.pago_set_code(buf, l, int(want[l]))
+    assert [L.pago_code_at(buf, l) for l in range(16)] == list(want)
+    L.pago_set_code(buf, 5, 3)
+    assert L.pago_code_at(buf, 5) == 3 and L.pago_code_at(buf, 4) == want[4] and L.pago_code_at(buf, 6) == want[6]
+
+
+def test_reference_set_determinism_and_validation():  # test_projection.cpp:56-64, :96-100
+    L = O.lib()
+    a = np.zeros(64 * 16, np.float32)
+    b = np.zeros_like(a)
+    c = np.zeros_like(a)
+    assert L.pago_build_reference_set(64, 8, 16, 99, a) == 0
+    L.pago_build_reference_set(64, 8, 16, 99, b)
+    L.pago_build_reference_set(64, 8, 16, 100, c)
+    assert np.array_equal(a, b) and not np.array_equal(a, c)
+    big = np.zeros(64 * 64 * 17, np.float32)
+    assert L.pago_build_reference_set(64, 7, 16, 1, big) == 1
+    assert L.pago_build_reference_set(64, 64, 16, 1, big) == 1
+    assert L.pago_build_reference_set(64, 8, 17, 1, big) == 1
+    # antipodal layout at sub_dim 8, m 16 (test_projection.cpp:66-94)
+    r = a.reshape(8, 16, 8)
+    assert np.allclose(r[:, :8], -r[:, 8:], atol=1e-6)
+    assert np.allclose(np.linalg.norm(r, axis=2), 1 / np.sqrt(8), rtol=1e-5)
+
+
+def test_default_subspace_count_kat():  # test_projection.cpp:210-222
+    L = O.lib()
+    assert [L.pago_default_subspace_count(d) for d in (64, 128, 256, 960, 1024)] == [8, 16, 16, 32, 32]
+    for d in (64, 128, 200, 256, 960, 1024):
+        assert d // L.pago_default_subspace_count(d) >= 4
+
+
+def test_mt19937_64_and_normal_streams():
+    """libstdc++ RNG restatement: the C++ standard's KAT (10000th output of a
+    default-seeded mt19937_64) and the reference family regenerated from it
+    (checked bit-exactly against the reference in test_tables_and_refs)."""
+    out = np.zeros(10000, np.uint64)
+    O.lib().pago_mt64_stream(5489, out, 10000)
+    assert int(out[-1]) == 9981545732273789042
+    z = np.zeros(200000, np.float64)
+    O.lib().pago_normal_stream(1, z, z.size)
+    assert abs(z.mean()) < 0.01 and abs(z.std() - 1) < 0.01
+
+
+def test_sq_dist_kats():  # test_vecstore.cpp:58-88
+    L = O.lib()
+    rng = np.random.default_rng(7)
+    for n in (1, 3, 8, 17, 64, 100, 257):
+        a = rng.standard_normal(n).astype(np.float32)
+        b = rng.standard_normal(n).astype(np.float32)
+        want = float(((a.astype(np.float64) - b) ** 2).sum())
+        assert abs(L.pago_sq_dist(a, b, n) - want) <= 1e-4 * max(1.0, want)
+        assert abs(L.pago_vec_norm(a, n) - np.linalg.norm(a.astype(np.float64))) <= 1e-5 * max(1, np.linalg.norm(a))
+    a = rng.standard_normal(96).astype(np.float32)
+    b = rng.standard_normal(96).astype(np.float32)
+    ab = L.pago_sq_dist(a, b, 96)
+    assert L.pago_sq_dist(b, a, 96) == ab and L.pago_sq_dist(a, a, 96) == 0.0
+
+
+def test_ground_truth_vs_hand_scan():  # test_bench.cpp:14-47
+    rng = np.random.default_rng(700)
+    base = rng.standard_normal((50, 6)).astype(np.float32)
+    q = rng.standard_normal((5, 6)).astype(np.float32)
+    ids, sq = O.ground_truth(base, q, 7)
+    L = O.lib()
+    for i in range(5):
+        d = np.array([L.pago_sq_dist(base[j].copy(), q[i].copy(), 6) for j in range(50)], np.float32)
+        order = sorted(range(50), key=lambda j: (d[j], j))[:7]
+        assert list(ids[i]) == order and np.array_equal(sq[i], d[order])
+    ids, sq = O.ground_truth(base[:4], q, 7)  # k > n -> k = n
+    assert ids.shape == (5, 4)
+
+
+def test_recall_tie_policy_kat():  # test_bench.cpp:49-67
+    t_ids = np.array([0, 1, 2, 3, 4], np.uint32)
+    t_sq = np.array([1, 2, 3, 3, 9], np.float32)
+    r = lambda ids: O.recall_at_k(np.array(ids, np.uint32), t_ids, t_sq, 3)  # noqa: E731
+    assert r([0, 1, 2]) == 1.0 and abs(r([0, 1, 42]) - 2 / 3) < 1e-12
+    assert r([0, 1, 3]) == 1.0 and abs(r([0, 1, 4]) - 2 / 3) < 1e-12
