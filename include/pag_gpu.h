@@ -95,7 +95,7 @@ int pag_gpu_search(pag_gpu_index* ix, const float* q, uint64_t nq,
 /* Same engine with every buffer already on device 0 of the handle
  * (q_dev: nq x dim fp32, ids/sq: nq x K, n_out: nq, stats_dev: nq x 8 u32
  * raw counters {exact,test,pass,visited,edges,status,marks,0}), launched on
- * `stream` (a cudaStream_t; NULL = the handle's stream) without host
+ * `stream` (a cudaStream_t; NULL = the legacy default stream) without host
  * synchronisation. For resident-input throughput measurement and for
  * callers that keep queries on the GPU. Queries flagged with a visited-set
  * overflow (status bit 1) are NOT retried on this path. */

@@ -82,8 +82,10 @@ struct SearchLaunch {
 };
 
 size_t search_kernel_smem(const SearchLaunch& L);
+// b <= 32: working set and rings in registers (no smem for them)
+bool search_uses_registers(const SearchLaunch& L);
 cudaError_t launch_search(const SearchLaunch& L, int grid, cudaStream_t stream);
-cudaError_t search_occupancy(int warps_per_block, size_t smem_bytes, int* blocks_per_sm);
+cudaError_t search_occupancy(const SearchLaunch& L, int* blocks_per_sm);
 
 // Exact brute-force ground truth (bench.cpp:18-53): reference-order fp32
 // distances, top-k by (sq, id).

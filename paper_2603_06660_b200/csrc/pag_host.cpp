@@ -476,7 +476,7 @@ struct Plan {
 };
 
 constexpr int kWarpsPerBlock = 4;
-constexpr uint32_t kWarpSmemBudget = 20 * 1024;
+constexpr uint32_t kWarpSmemBudget = 14 * 1024;
 
 uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 
@@ -494,9 +494,10 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     L.nq = nq;
     L.ix = ix.view(r);
     L.warps_per_block = kWarpsPerBlock;
-    L.stage_rows = 8;
+    L.stage_rows = 4;
     L.hash_log2 = p.efS <= 200 ? 10 : 11;
     const uint32_t b = L.b, capr = std::max(1u, p.efS);
+    const bool regs = pagdev::search_uses_registers(L);
     // fixed smem regions
     uint32_t off = 0;
     L.off_q = off;
@@ -508,10 +509,11 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     L.off_sqbuf = off;
     off = align16(off + 256);
     L.off_stage = off;
-    off = align16(off + 4 * 132 * L.stage_rows);
-    // movable regions: W (12b), rings (24b), R_L (24 capr), merge (48b)
-    const uint64_t szW = align16(12 * b), szR = align16(24 * b), szRL = align16(24 * capr),
-                   szM = align16(48 * b);
+    off = align16(off + 4 * 36 * 16);
+    // movable regions: W (12b), rings (24b), R_L (24 capr), merge (48b);
+    // with b <= 32 the working set and rings live in registers
+    const uint64_t szW = regs ? 0 : align16(12 * b), szR = regs ? 0 : align16(24 * b),
+                   szRL = align16(24 * capr), szM = align16(48 * b);
     bool w_s = true, r_s = true, rl_s = true, m_s = true;
     auto total = [&]() {
         return off + (w_s ? szW : 0) + (r_s ? szR : 0) + (rl_s ? szRL : 0) + (m_s ? szM : 0);
@@ -532,10 +534,8 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
         }
     };
     place(w_s, szW, &L.off_W, &L.W_in_smem);
-    uint32_t dummy;
     place(r_s, szR, &L.off_rf, &L.rings_in_smem);
     L.off_rt = L.off_rf + 12 * b;
-    (void)dummy;
     place(rl_s, szRL, &L.off_rl, &L.rl_in_smem);
     place(m_s, szM, &L.off_merge, &L.merge_in_smem);
     L.warp_smem_bytes = align16(off);
@@ -549,8 +549,7 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
         if (forced >= 4 && forced < 28) L.gtab_log2 = std::max(forced, gt_log2_min);
     }
     int bps = 0;
-    size_t smem = static_cast<size_t>(L.warp_smem_bytes) * kWarpsPerBlock;
-    cuda_check(pagdev::search_occupancy(kWarpsPerBlock, smem, &bps), "occupancy");
+    cuda_check(pagdev::search_occupancy(L, &bps), "occupancy");
     if (bps <= 0) throw_err(PAG_GPU_ERUNTIME, "search configuration does not fit on the GPU");
     const int want_blocks = static_cast<int>((nq + kWarpsPerBlock - 1) / kWarpsPerBlock);
     pl.grid = std::max(1, std::min(r.num_sms * bps, want_blocks));
@@ -569,8 +568,8 @@ void ensure_scratch(Replica& r, Plan& pl) {
         r.slot_epoch = nullptr;
         dev_alloc(&r.gtab, (ns << L.gtab_log2) * 8);
         dev_alloc(&r.slot_epoch, ns * 4);
-        cuda_check(cudaMemsetAsync(r.gtab, 0, (ns << L.gtab_log2) * 8, r.stream), "memset");
-        cuda_check(cudaMemsetAsync(r.slot_epoch, 0, ns * 4, r.stream), "memset");
+        cuda_check(cudaMemset(r.gtab, 0, (ns << L.gtab_log2) * 8), "memset");  // blocking: any stream may follow
+        cuda_check(cudaMemset(r.slot_epoch, 0, ns * 4), "memset");
         r.slots = ns;
         r.gtab_log2 = L.gtab_log2;
     }
@@ -845,7 +844,7 @@ int pag_gpu_search_device(pag_gpu_index* ix, const float* q_dev, uint64_t nq,
         validate_params(*ix, p);
         Replica& r = ix->reps[0];
         cuda_check(cudaSetDevice(r.device), "cudaSetDevice");
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : r.stream;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
         if (nq >= 0xFFFFFFFFull) throw_err(PAG_GPU_EINVAL, "batch too large");
         run_search(*ix, r, p, q_dev, static_cast<uint32_t>(nq), nullptr, ids_dev, sq_dev, n_out_dev,
                    stats_dev, s, 0);

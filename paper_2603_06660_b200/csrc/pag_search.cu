@@ -19,9 +19,16 @@
 //         expansion and the test is monotone in it, so this set is a
 //         superset of the reference's passes);
 //   (ii)  __ballot_sync compaction of the survivors;
-//   (iii) their exact distances, batched 8 rows per warp;
+//   (iii) their exact distances (rows prefetched to L2 by bulk copy, streamed
+//         in 128-float chunks with one chunk of look-ahead);
 //   (iv)  an in-order replay re-evaluating the PRT with the live radius
 //         before marking and admitting / pushing to R_F.
+//
+// Two state layouts share the code (template parameter TFB):
+//   TfbReg  (b <= 32, K <= 32): the working set W and both FIFO rings live in
+//           registers, slot i on lane i; argmin/argmax are __reduce_*_sync.
+//   TfbMem  (b > 32): W and rings as arrays in smem or the warp's HBM slot.
+// R_L (capacity efS) is an array in smem, or HBM when it does not fit.
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
@@ -34,12 +41,16 @@ namespace {
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint32_t EMPTY = 0xffffffffu;
 constexpr uint32_t VISITED = 0x80000000u;
-constexpr int STAGE_STRIDE = 132;  // floats per staged row chunk (bank-conflict-free)
-constexpr int MAX_STAGE_ROWS = 8;
+constexpr int XSTR = 36;        // floats per transposed chain row in the staging buffer
+constexpr int EXACT_ROWS = 4;   // rows per exact-distance batch (16 chain lanes)
+constexpr int FAST_ROWS = 8;    // rows per warp-tree batch
 
 __device__ __forceinline__ bool cless(float sa, uint32_t ia, float sb, uint32_t ib) {
     return sa < sb || (sa == sb && ia < ib);  // candidate_less, builder.hpp:23-25
 }
+
+// order-preserving key of a non-negative float (-0 folds onto +0)
+__device__ __forceinline__ uint32_t fkey(float x) { return __float_as_uint(__fadd_rn(x, 0.0f)); }
 
 // routing.hpp:40-43 — ((e*e + d*d) - z*z) / ((2*d)*e), no contraction
 __device__ __forceinline__ float prt_threshold(float en, float duq, float dz) {
@@ -74,201 +85,128 @@ __device__ __forceinline__ Arr make_arr(uint8_t* base, uint32_t cap) {
     return a;
 }
 
-// Per-warp search state. Scalars are warp-uniform registers; arrays are
-// generic pointers into this warp's smem region or its HBM slot.
-struct Tfb {
-    Arr W;                 // working set, cap b (aux = deg | VISITED)
-    Arr rf, rt;            // FIFO rings, cap b (aux = deg)
-    Arr rlA, rlB;          // result list double buffer, cap efS (aux unused)
-    Arr mi, mo;            // merge scratch, cap 2b
-    uint32_t b, cap_r;
-    uint32_t wsize;
-    float zmax_sq, zmax_dist;
-    uint32_t zmax_idx;
-    uint32_t rf_head, rf_size, rt_head, rt_size;
-    uint32_t rl_cur, rl_size;
-    // visited set
+// ---------------------------------------------------------------------------
+// Per-warp state shared by both TFB layouts: query, projection table, visited
+// set, result list, counters.
+// ---------------------------------------------------------------------------
+struct Common {
+    float* q;
+    float* T;
+    float* stage;
+    float* sqbuf;
+    uint32_t* degbuf;
+    // visited marks (routing.hpp:104-105): smem open addressing, spilling to
+    // an epoch-stamped per-slot HBM table once the smem table is half full
     uint32_t* hs;
     uint32_t hs_log2, hs_count;
     uint64_t* gt;
     uint32_t gt_log2, gt_count, epoch;
     bool gt_used, overflow;
-    // counters
+    // R_L double buffer (cap efS) and a scratch array (cap 2b)
+    Arr rlA, rlB, mo;
+    uint32_t rl_cur, rl_size, cap_r;
+    // counters (routing.hpp:24-34 + edges_scanned)
     uint32_t n_exact, n_test, n_pass, n_visited, n_edges;
 
     __device__ Arr rl_cur_arr() const { return rl_cur ? rlB : rlA; }
     __device__ Arr rl_next_arr() const { return rl_cur ? rlA : rlB; }
-    __device__ float admission_sq() const { return wsize < b ? CUDART_INF_F : zmax_sq; }
-    __device__ float admission_dist() const { return wsize < b ? CUDART_INF_F : zmax_dist; }
 };
 
-// ---- visited marks (routing.hpp:104-105): smem open addressing, spilling
-// to an epoch-stamped per-slot HBM table once the smem table is half full.
-__device__ __forceinline__ bool marked(const Tfb& s, uint32_t id) {
-    const uint32_t mask = (1u << s.hs_log2) - 1;
-    uint32_t h = hslot(id, s.hs_log2);
+__device__ __forceinline__ bool marked(const Common& c, uint32_t id) {
+    const uint32_t mask = (1u << c.hs_log2) - 1;
+    uint32_t h = hslot(id, c.hs_log2);
     while (true) {
-        uint32_t v = s.hs[h];
+        const uint32_t v = c.hs[h];
         if (v == id) return true;
         if (v == EMPTY) break;
         h = (h + 1) & mask;
     }
-    if (!s.gt_used) return false;
-    const uint32_t gm = (1u << s.gt_log2) - 1;
-    h = hslot(id, s.gt_log2);
+    if (!c.gt_used) return false;
+    const uint32_t gm = (1u << c.gt_log2) - 1;
+    h = hslot(id, c.gt_log2);
     while (true) {
-        uint64_t e = s.gt[h];
-        if (static_cast<uint32_t>(e >> 32) != s.epoch) return false;
+        const uint64_t e = c.gt[h];
+        if (static_cast<uint32_t>(e >> 32) != c.epoch) return false;
         if (static_cast<uint32_t>(e) == id) return true;
         h = (h + 1) & gm;
     }
 }
 
-// warp-uniform call; one lane writes
-__device__ __forceinline__ void mark(Tfb& s, uint32_t id, int lane) {
-    if (s.hs_count < (1u << s.hs_log2) / 2) {
+// warp-uniform call; lane 0 writes
+__device__ __forceinline__ void mark(Common& c, uint32_t id, int lane) {
+    if (c.hs_count < (1u << c.hs_log2) / 2) {
         if (lane == 0) {
-            const uint32_t mask = (1u << s.hs_log2) - 1;
-            uint32_t h = hslot(id, s.hs_log2);
-            while (s.hs[h] != EMPTY) h = (h + 1) & mask;
-            s.hs[h] = id;
+            const uint32_t mask = (1u << c.hs_log2) - 1;
+            uint32_t h = hslot(id, c.hs_log2);
+            while (c.hs[h] != EMPTY) h = (h + 1) & mask;
+            c.hs[h] = id;
         }
-        ++s.hs_count;
+        ++c.hs_count;
     } else {
-        const uint32_t cap = 1u << s.gt_log2;
-        if (s.gt_count + 1 >= cap - cap / 4) {
-            s.overflow = true;  // host re-runs this query with a larger table
+        const uint32_t cap = 1u << c.gt_log2;
+        if (c.gt_count + 1 >= cap - cap / 4) {
+            c.overflow = true;  // host re-runs this query with a larger table
             return;
         }
         if (lane == 0) {
             const uint32_t gm = cap - 1;
-            uint32_t h = hslot(id, s.gt_log2);
-            while (static_cast<uint32_t>(s.gt[h] >> 32) == s.epoch) h = (h + 1) & gm;
-            s.gt[h] = (static_cast<uint64_t>(s.epoch) << 32) | id;
+            uint32_t h = hslot(id, c.gt_log2);
+            while (static_cast<uint32_t>(c.gt[h] >> 32) == c.epoch) h = (h + 1) & gm;
+            c.gt[h] = (static_cast<uint64_t>(c.epoch) << 32) | id;
         }
-        s.gt_used = true;
-        ++s.gt_count;
+        c.gt_used = true;
+        ++c.gt_count;
     }
     __syncwarp();
 }
 
-// ---- routing.cpp:32-44: argmax sq over W, first slot on ties
-__device__ void recompute_zmax(Tfb& s, int lane) {
-    if (s.wsize == 0) {
-        s.zmax_sq = s.zmax_dist = 0.0f;
-        s.zmax_idx = 0;
-        return;
+// number of entries of sorted a[0..n) strictly less than (v, id)
+__device__ __forceinline__ uint32_t count_less(const Arr& a, uint32_t n, float v, uint32_t id) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (cless(a.sq[mid], a.id[mid], v, id))
+            lo = mid + 1;
+        else
+            hi = mid;
     }
-    float bs = -CUDART_INF_F;
-    uint32_t bi = EMPTY;
-    for (uint32_t i = lane; i < s.wsize; i += 32) {
-        float v = s.W.sq[i];
-        if (bi == EMPTY || v > bs) {
-            bs = v;
-            bi = i;
-        }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        float v2 = __shfl_xor_sync(FULL, bs, o);
-        uint32_t i2 = __shfl_xor_sync(FULL, bi, o);
-        if (i2 != EMPTY && (bi == EMPTY || v2 > bs || (v2 == bs && i2 < bi))) {
-            bs = v2;
-            bi = i2;
-        }
-    }
-    s.zmax_idx = bi;
-    s.zmax_sq = bs;
-    s.zmax_dist = __fsqrt_rn(bs);
+    return lo;
 }
 
-// ---- routing.cpp:71-80: argmin over unvisited W by (sq, id); EMPTY if none
-__device__ uint32_t next_unvisited(const Tfb& s, int lane) {
-    float bs = CUDART_INF_F;
-    uint32_t bid = EMPTY, bslot = EMPTY;
-    for (uint32_t i = lane; i < s.wsize; i += 32) {
-        if (s.W.aux[i] & VISITED) continue;
-        float v = s.W.sq[i];
-        uint32_t id = s.W.id[i];
-        if (bslot == EMPTY || cless(v, id, bs, bid)) {
-            bs = v;
-            bid = id;
-            bslot = i;
+// routing.cpp:82-90 applied to a sorted batch: R_L keeps the cap_r smallest
+// (the bounded sorted insert is order-independent for distinct ids).
+__device__ void rl_merge(Common& c, const Arr& batch, uint32_t nb, int lane) {
+    if (nb == 0) return;
+    const Arr cur = c.rl_cur_arr(), nxt = c.rl_next_arr();
+    const uint32_t cap = c.cap_r;
+    for (uint32_t i = lane; i < c.rl_size; i += 32) {
+        const float v = cur.sq[i];
+        const uint32_t id = cur.id[i];
+        const uint32_t pos = i + count_less(batch, nb, v, id);
+        if (pos < cap) {
+            nxt.id[pos] = id;
+            nxt.sq[pos] = v;
         }
     }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        float v2 = __shfl_xor_sync(FULL, bs, o);
-        uint32_t id2 = __shfl_xor_sync(FULL, bid, o);
-        uint32_t sl2 = __shfl_xor_sync(FULL, bslot, o);
-        if (sl2 != EMPTY && (bslot == EMPTY || cless(v2, id2, bs, bid))) {
-            bs = v2;
-            bid = id2;
-            bslot = sl2;
+    for (uint32_t j = lane; j < nb; j += 32) {
+        const float v = batch.sq[j];
+        const uint32_t id = batch.id[j];
+        const uint32_t pos = j + count_less(cur, c.rl_size, v, id);
+        if (pos < cap) {
+            nxt.id[pos] = id;
+            nxt.sq[pos] = v;
         }
-    }
-    return bslot;
-}
-
-// ---- ring push (routing.hpp:79-86), one lane writes
-__device__ __forceinline__ void ring_push(const Arr& r, uint32_t cap, uint32_t& head,
-                                          uint32_t& size, uint32_t id, float sq, uint32_t aux,
-                                          int lane) {
-    uint32_t pos = head + size;
-    if (pos >= cap) pos -= cap;
-    if (lane == 0) {
-        r.id[pos] = id;
-        r.sq[pos] = sq;
-        r.aux[pos] = aux;
-    }
-    if (size < cap) {
-        ++size;
-    } else {
-        head = (head + 1 == cap) ? 0 : head + 1;
-    }
-}
-
-// ---- routing.cpp:46-53 (seed) and :55-69 (admit)
-__device__ __forceinline__ void w_append(Tfb& s, uint32_t id, float sq, uint32_t deg, int lane) {
-    if (lane == 0) {
-        s.W.id[s.wsize] = id;
-        s.W.sq[s.wsize] = sq;
-        s.W.aux[s.wsize] = deg;
-    }
-    ++s.wsize;
-    if (sq > s.zmax_sq || s.wsize == 1) {
-        s.zmax_idx = s.wsize - 1;
-        s.zmax_sq = sq;
-        s.zmax_dist = __fsqrt_rn(sq);
-    }
-}
-
-__device__ void admit(Tfb& s, uint32_t id, float sq, uint32_t deg, int lane) {
-    if (s.wsize < s.b) {
-        w_append(s, id, sq, deg, lane);
-        __syncwarp();
-        return;
-    }
-    const uint32_t z = s.zmax_idx;
-    uint32_t oid = s.W.id[z];
-    float osq = s.W.sq[z];
-    uint32_t oaux = s.W.aux[z] & ~VISITED;
-    __syncwarp();
-    ring_push(s.rt, s.b, s.rt_head, s.rt_size, oid, osq, oaux, lane);
-    if (lane == 0) {
-        s.W.id[z] = id;
-        s.W.sq[z] = sq;
-        s.W.aux[z] = deg;
     }
     __syncwarp();
-    recompute_zmax(s, lane);
+    c.rl_size = min(cap, c.rl_size + nb);
+    c.rl_cur ^= 1;
 }
 
-// rank sort of n entries (distinct ids => strict total order)
+// rank sort of n array entries (distinct ids => strict total order)
 __device__ void rank_sort(const Arr& in, const Arr& out, uint32_t n, int lane) {
     for (uint32_t i = lane; i < n; i += 32) {
-        float v = in.sq[i];
-        uint32_t id = in.id[i];
+        const float v = in.sq[i];
+        const uint32_t id = in.id[i];
         uint32_t r = 0;
         for (uint32_t j = 0; j < n; ++j) r += cless(in.sq[j], in.id[j], v, id) ? 1u : 0u;
         out.id[r] = id;
@@ -278,198 +216,490 @@ __device__ void rank_sort(const Arr& in, const Arr& out, uint32_t n, int lane) {
     __syncwarp();
 }
 
-// number of entries of sorted a[0..n) strictly less than (v, id)
-__device__ __forceinline__ uint32_t count_less(const Arr& a, uint32_t n, float v, uint32_t id) {
-    uint32_t lo = 0, hi = n;
-    while (lo < hi) {
-        uint32_t mid = (lo + hi) >> 1;
-        if (cless(a.sq[mid], a.id[mid], v, id))
-            lo = mid + 1;
-        else
-            hi = mid;
-    }
-    return lo;
-}
+// ---------------------------------------------------------------------------
+// TfbReg: b <= 32. Lane i holds W slot i, ring_f physical slot i and ring_t
+// physical slot i (routing.hpp:62-161 with the reference's slot placement).
+// ---------------------------------------------------------------------------
+struct TfbReg {
+    uint32_t b;
+    uint32_t w_id, w_deg;
+    float w_sq;
+    bool w_vis;
+    uint32_t f_id, f_deg;
+    float f_sq;
+    uint32_t t_id, t_deg;
+    float t_sq;
+    uint32_t wsize, rf_head, rf_size, rt_head, rt_size;
+    float zmax_sq, zmax_dist;
+    uint32_t zmax_idx;
 
-// routing.cpp:82-90 applied to a whole batch: R_L keeps the cap_r smallest
-// (the bounded sorted insert is order-independent for distinct ids).
-// `batch` must be sorted.
-__device__ void rl_merge(Tfb& s, const Arr& batch, uint32_t nb, int lane) {
-    if (nb == 0) return;
-    const Arr cur = s.rl_cur_arr(), nxt = s.rl_next_arr();
-    const uint32_t cap = s.cap_r;
-    for (uint32_t i = lane; i < s.rl_size; i += 32) {
-        float v = cur.sq[i];
-        uint32_t id = cur.id[i];
-        uint32_t pos = i + count_less(batch, nb, v, id);
-        if (pos < cap) {
-            nxt.id[pos] = id;
-            nxt.sq[pos] = v;
+    __device__ void init(uint32_t b_, uint8_t*, uint8_t*, const SearchLaunch&) { b = b_; }
+    __device__ void reset() {
+        wsize = rf_head = rf_size = rt_head = rt_size = 0;
+        zmax_sq = zmax_dist = 0.0f;
+        zmax_idx = 0;
+        w_vis = false;
+    }
+    __device__ float admission_sq() const { return wsize < b ? CUDART_INF_F : zmax_sq; }
+    __device__ float admission_dist() const { return wsize < b ? CUDART_INF_F : zmax_dist; }
+
+    // routing.cpp:32-44: argmax, first slot on ties
+    __device__ void recompute_zmax(int lane) {
+        if (wsize == 0) {
+            zmax_sq = zmax_dist = 0.0f;
+            zmax_idx = 0;
+            return;
+        }
+        const bool v = static_cast<uint32_t>(lane) < wsize;
+        const uint32_t k = v ? fkey(w_sq) : 0u;
+        const uint32_t m = __reduce_max_sync(FULL, k);
+        zmax_idx = __ffs(__ballot_sync(FULL, v && k == m)) - 1;
+        zmax_sq = __shfl_sync(FULL, w_sq, zmax_idx);
+        zmax_dist = __fsqrt_rn(zmax_sq);
+    }
+    // routing.cpp:71-80: argmin over unvisited by (sq, id); `skip` excluded
+    __device__ uint32_t next_unvisited(int lane, uint32_t skip = EMPTY) const {
+        const bool v = static_cast<uint32_t>(lane) < wsize && !w_vis && static_cast<uint32_t>(lane) != skip;
+        if (!__ballot_sync(FULL, v)) return EMPTY;
+        const uint32_t k = v ? fkey(w_sq) : 0xffffffffu;
+        const uint32_t m1 = __reduce_min_sync(FULL, k);
+        const bool c1 = v && k == m1;
+        const uint32_t m2 = __reduce_min_sync(FULL, c1 ? w_id : 0xffffffffu);
+        return __ffs(__ballot_sync(FULL, c1 && w_id == m2)) - 1;
+    }
+    __device__ void entry(uint32_t slot, uint32_t& id, float& sq, uint32_t& deg) const {
+        id = __shfl_sync(FULL, w_id, slot);
+        sq = __shfl_sync(FULL, w_sq, slot);
+        deg = __shfl_sync(FULL, w_deg, slot);
+    }
+    __device__ uint32_t entry_id(uint32_t slot) const { return __shfl_sync(FULL, w_id, slot); }
+    __device__ uint32_t entry_deg(uint32_t slot) const { return __shfl_sync(FULL, w_deg, slot); }
+    __device__ void set_visited(uint32_t slot, int lane) {
+        if (static_cast<uint32_t>(lane) == slot) w_vis = true;
+    }
+    // routing.cpp:46-53 / :57-63
+    __device__ void append(uint32_t id, float sq, uint32_t deg, int lane) {
+        if (static_cast<uint32_t>(lane) == wsize) {
+            w_id = id;
+            w_sq = sq;
+            w_deg = deg;
+            w_vis = false;
+        }
+        ++wsize;
+        if (sq > zmax_sq || wsize == 1) {
+            zmax_idx = wsize - 1;
+            zmax_sq = sq;
+            zmax_dist = __fsqrt_rn(sq);
         }
     }
-    for (uint32_t j = lane; j < nb; j += 32) {
-        float v = batch.sq[j];
-        uint32_t id = batch.id[j];
-        uint32_t pos = j + count_less(cur, s.rl_size, v, id);
-        if (pos < cap) {
-            nxt.id[pos] = id;
-            nxt.sq[pos] = v;
+    __device__ void push_rt(uint32_t id, float sq, uint32_t deg, int lane) {
+        uint32_t pos = rt_head + rt_size;
+        if (pos >= b) pos -= b;
+        if (static_cast<uint32_t>(lane) == pos) {
+            t_id = id;
+            t_sq = sq;
+            t_deg = deg;
         }
+        if (rt_size < b) ++rt_size;
+        else rt_head = (rt_head + 1 == b) ? 0 : rt_head + 1;
     }
-    __syncwarp();
-    s.rl_size = min(cap, s.rl_size + nb);
-    s.rl_cur ^= 1;
-}
-
-// flush W into R_L (routing.cpp:93, :242)
-__device__ void flush_working(Tfb& s, int lane) {
-    rank_sort(s.W, s.mo, s.wsize, lane);
-    rl_merge(s, s.mo, s.wsize, lane);
-}
-
-// routing.cpp:92-114
-__device__ bool end_round(Tfb& s, int lane) {
-    flush_working(s, lane);
-    s.wsize = 0;
-    uint32_t nm = 0;
-    for (uint32_t i = lane; i < s.rf_size; i += 32) {
-        uint32_t p = s.rf_head + i;
-        if (p >= s.b) p -= s.b;
-        s.mi.id[i] = s.rf.id[p];
-        s.mi.sq[i] = s.rf.sq[p];
-        s.mi.aux[i] = s.rf.aux[p];
-    }
-    nm = s.rf_size;
-    for (uint32_t i = lane; i < s.rt_size; i += 32) {
-        uint32_t p = s.rt_head + i;
-        if (p >= s.b) p -= s.b;
-        s.mi.id[nm + i] = s.rt.id[p];
-        s.mi.sq[nm + i] = s.rt.sq[p];
-        s.mi.aux[nm + i] = s.rt.aux[p];
-    }
-    nm += s.rt_size;
-    s.rf_head = s.rf_size = 0;
-    s.rt_head = s.rt_size = 0;
-    __syncwarp();
-    if (nm == 0) {
-        s.zmax_sq = s.zmax_dist = 0.0f;
-        return false;
-    }
-    rank_sort(s.mi, s.mo, nm, lane);
-    const uint32_t refill = min(nm, s.b);
-    for (uint32_t i = lane; i < nm; i += 32) {
-        if (i < refill) {
-            s.W.id[i] = s.mo.id[i];
-            s.W.sq[i] = s.mo.sq[i];
-            s.W.aux[i] = s.mo.aux[i];
-        } else {
-            uint32_t p = i - refill;  // ring_t was cleared and rest <= b
-            s.rt.id[p] = s.mo.id[i];
-            s.rt.sq[p] = s.mo.sq[i];
-            s.rt.aux[p] = s.mo.aux[i];
+    __device__ void push_fp(uint32_t id, float sq, uint32_t deg, int lane) {  // routing.hpp:128
+        uint32_t pos = rf_head + rf_size;
+        if (pos >= b) pos -= b;
+        if (static_cast<uint32_t>(lane) == pos) {
+            f_id = id;
+            f_sq = sq;
+            f_deg = deg;
         }
+        if (rf_size < b) ++rf_size;
+        else rf_head = (rf_head + 1 == b) ? 0 : rf_head + 1;
     }
-    s.wsize = refill;
-    s.rt_size = nm - refill;
-    __syncwarp();
-    recompute_zmax(s, lane);
-    return true;
-}
+    // routing.cpp:55-69
+    __device__ void admit(uint32_t id, float sq, uint32_t deg, int lane) {
+        if (wsize < b) {
+            append(id, sq, deg, lane);
+            return;
+        }
+        const uint32_t z = zmax_idx;
+        const uint32_t oid = __shfl_sync(FULL, w_id, z);
+        const float osq = __shfl_sync(FULL, w_sq, z);
+        const uint32_t odeg = __shfl_sync(FULL, w_deg, z);
+        push_rt(oid, osq, odeg, lane);
+        if (static_cast<uint32_t>(lane) == z) {
+            w_id = id;
+            w_sq = sq;
+            w_deg = deg;
+            w_vis = false;
+        }
+        recompute_zmax(lane);
+    }
+    // W -> R_L (routing.cpp:93 and :242)
+    __device__ void flush(Common& c, int lane) {
+        const bool v = static_cast<uint32_t>(lane) < wsize;
+        uint32_t r = 0;
+        for (uint32_t j = 0; j < wsize; ++j) {
+            const float sj = __shfl_sync(FULL, w_sq, j);
+            const uint32_t ij = __shfl_sync(FULL, w_id, j);
+            r += cless(sj, ij, w_sq, w_id) ? 1u : 0u;
+        }
+        if (v) {
+            c.mo.id[r] = w_id;
+            c.mo.sq[r] = w_sq;
+        }
+        __syncwarp();
+        rl_merge(c, c.mo, wsize, lane);
+    }
+    // routing.cpp:92-114
+    __device__ bool end_round(Common& c, int lane) {
+        flush(c, lane);
+        wsize = 0;
+        const uint32_t L = static_cast<uint32_t>(lane);
+        const bool fv = L < b && ((L + b - rf_head) % b) < rf_size;
+        const bool tv = L < b && ((L + b - rt_head) % b) < rt_size;
+        const uint32_t nm = rf_size + rt_size;
+        rf_head = rf_size = rt_head = rt_size = 0;
+        if (nm == 0) {
+            zmax_sq = zmax_dist = 0.0f;
+            return false;
+        }
+        uint32_t fr = 0, tr = 0;
+        for (uint32_t j = 0; j < b; ++j) {
+            const bool fvj = __shfl_sync(FULL, fv, j);
+            const bool tvj = __shfl_sync(FULL, tv, j);
+            const float fs = __shfl_sync(FULL, f_sq, j), ts = __shfl_sync(FULL, t_sq, j);
+            const uint32_t fi = __shfl_sync(FULL, f_id, j), ti = __shfl_sync(FULL, t_id, j);
+            if (fvj) {
+                fr += cless(fs, fi, f_sq, f_id) ? 1u : 0u;
+                tr += cless(fs, fi, t_sq, t_id) ? 1u : 0u;
+            }
+            if (tvj) {
+                fr += cless(ts, ti, f_sq, f_id) ? 1u : 0u;
+                tr += cless(ts, ti, t_sq, t_id) ? 1u : 0u;
+            }
+        }
+        __syncwarp();
+        if (fv) {
+            c.mo.id[fr] = f_id;
+            c.mo.sq[fr] = f_sq;
+            c.mo.aux[fr] = f_deg;
+        }
+        if (tv) {
+            c.mo.id[tr] = t_id;
+            c.mo.sq[tr] = t_sq;
+            c.mo.aux[tr] = t_deg;
+        }
+        __syncwarp();
+        const uint32_t refill = min(nm, b);
+        if (L < refill) {
+            w_id = c.mo.id[L];
+            w_sq = c.mo.sq[L];
+            w_deg = c.mo.aux[L];
+            w_vis = false;
+        }
+        if (L < nm - refill) {  // ring_t was cleared; the rest (<= b) in ascending order
+            t_id = c.mo.id[refill + L];
+            t_sq = c.mo.sq[refill + L];
+            t_deg = c.mo.aux[refill + L];
+        }
+        wsize = refill;
+        rt_size = nm - refill;
+        __syncwarp();
+        recompute_zmax(lane);
+        return true;
+    }
+};
 
-// ---- exact squared distances for the rows named by lanes in `items`
-// (lane j: row id w). Results land in sqbuf[j] (and deg[w] in degbuf[j]).
-// exact=1: the reference order (vecstore.cpp:77-95) — rows are streamed
-// coalesced in 128-float chunks, squared differences staged in smem, and
-// 4 lanes per row run the four strided accumulator chains serially.
-// exact=0: lane-parallel FMA partials + xor-tree (ablation / fast mode).
-__device__ void distances(const SearchLaunch& P, uint32_t items, uint32_t w, const float* q,
-                          float* stage, float* sqbuf, uint32_t* degbuf, int lane) {
+// ---------------------------------------------------------------------------
+// TfbMem: b > 32. Arrays in smem or the warp's HBM slot.
+// ---------------------------------------------------------------------------
+struct TfbMem {
+    Arr W, rf, rt, mi;
+    uint32_t b;
+    uint32_t wsize, rf_head, rf_size, rt_head, rt_size;
+    float zmax_sq, zmax_dist;
+    uint32_t zmax_idx;
+
+    __device__ void init(uint32_t b_, uint8_t* sw, uint8_t* gw, const SearchLaunch& P) {
+        b = b_;
+        W = make_arr((P.W_in_smem ? sw : gw) + P.off_W, b);
+        rf = make_arr((P.rings_in_smem ? sw : gw) + P.off_rf, b);
+        rt = make_arr((P.rings_in_smem ? sw : gw) + P.off_rt, b);
+        mi = make_arr((P.merge_in_smem ? sw : gw) + P.off_merge, 2 * b);
+    }
+    __device__ void reset() {
+        wsize = rf_head = rf_size = rt_head = rt_size = 0;
+        zmax_sq = zmax_dist = 0.0f;
+        zmax_idx = 0;
+    }
+    __device__ float admission_sq() const { return wsize < b ? CUDART_INF_F : zmax_sq; }
+    __device__ float admission_dist() const { return wsize < b ? CUDART_INF_F : zmax_dist; }
+
+    __device__ void recompute_zmax(int lane) {
+        if (wsize == 0) {
+            zmax_sq = zmax_dist = 0.0f;
+            zmax_idx = 0;
+            return;
+        }
+        uint32_t bk = 0, bi = EMPTY;
+        for (uint32_t i = lane; i < wsize; i += 32) {
+            const uint32_t k = fkey(W.sq[i]);
+            if (bi == EMPTY || k > bk) {
+                bk = k;
+                bi = i;
+            }
+        }
+        const uint32_t m = __reduce_max_sync(FULL, bi == EMPTY ? 0u : bk);
+        zmax_idx = __reduce_min_sync(FULL, (bi != EMPTY && bk == m) ? bi : EMPTY);
+        zmax_sq = W.sq[zmax_idx];
+        zmax_dist = __fsqrt_rn(zmax_sq);
+    }
+    __device__ uint32_t next_unvisited(int lane, uint32_t skip = EMPTY) const {
+        uint32_t bk = 0xffffffffu, bid = EMPTY, bslot = EMPTY;
+        for (uint32_t i = lane; i < wsize; i += 32) {
+            if ((W.aux[i] & VISITED) || i == skip) continue;
+            const uint32_t k = fkey(W.sq[i]);
+            const uint32_t id = W.id[i];
+            if (bslot == EMPTY || k < bk || (k == bk && id < bid)) {
+                bk = k;
+                bid = id;
+                bslot = i;
+            }
+        }
+        const uint32_t m1 = __reduce_min_sync(FULL, bslot == EMPTY ? 0xffffffffu : bk);
+        const bool c1 = bslot != EMPTY && bk == m1;
+        if (!__ballot_sync(FULL, bslot != EMPTY)) return EMPTY;
+        const uint32_t m2 = __reduce_min_sync(FULL, c1 ? bid : 0xffffffffu);
+        return __reduce_min_sync(FULL, (c1 && bid == m2) ? bslot : EMPTY);
+    }
+    __device__ void entry(uint32_t slot, uint32_t& id, float& sq, uint32_t& deg) const {
+        id = W.id[slot];
+        sq = W.sq[slot];
+        deg = W.aux[slot] & ~VISITED;
+    }
+    __device__ uint32_t entry_id(uint32_t slot) const { return W.id[slot]; }
+    __device__ uint32_t entry_deg(uint32_t slot) const { return W.aux[slot] & ~VISITED; }
+    __device__ void set_visited(uint32_t slot, int lane) {
+        const uint32_t a = W.aux[slot];
+        __syncwarp();
+        if (lane == 0) W.aux[slot] = a | VISITED;
+        __syncwarp();
+    }
+    __device__ void append(uint32_t id, float sq, uint32_t deg, int lane) {
+        if (lane == 0) {
+            W.id[wsize] = id;
+            W.sq[wsize] = sq;
+            W.aux[wsize] = deg;
+        }
+        ++wsize;
+        if (sq > zmax_sq || wsize == 1) {
+            zmax_idx = wsize - 1;
+            zmax_sq = sq;
+            zmax_dist = __fsqrt_rn(sq);
+        }
+        __syncwarp();
+    }
+    __device__ static void ring_push(const Arr& r, uint32_t cap, uint32_t& head, uint32_t& size,
+                                     uint32_t id, float sq, uint32_t aux, int lane) {
+        uint32_t pos = head + size;
+        if (pos >= cap) pos -= cap;
+        if (lane == 0) {
+            r.id[pos] = id;
+            r.sq[pos] = sq;
+            r.aux[pos] = aux;
+        }
+        if (size < cap) ++size;
+        else head = (head + 1 == cap) ? 0 : head + 1;
+    }
+    __device__ void push_fp(uint32_t id, float sq, uint32_t deg, int lane) {
+        ring_push(rf, b, rf_head, rf_size, id, sq, deg, lane);
+        __syncwarp();
+    }
+    __device__ void admit(uint32_t id, float sq, uint32_t deg, int lane) {
+        if (wsize < b) {
+            append(id, sq, deg, lane);
+            return;
+        }
+        const uint32_t z = zmax_idx;
+        const uint32_t oid = W.id[z];
+        const float osq = W.sq[z];
+        const uint32_t oaux = W.aux[z] & ~VISITED;
+        __syncwarp();
+        ring_push(rt, b, rt_head, rt_size, oid, osq, oaux, lane);
+        if (lane == 0) {
+            W.id[z] = id;
+            W.sq[z] = sq;
+            W.aux[z] = deg;
+        }
+        __syncwarp();
+        recompute_zmax(lane);
+    }
+    __device__ void flush(Common& c, int lane) {
+        rank_sort(W, c.mo, wsize, lane);
+        rl_merge(c, c.mo, wsize, lane);
+    }
+    __device__ bool end_round(Common& c, int lane) {
+        flush(c, lane);
+        wsize = 0;
+        for (uint32_t i = lane; i < rf_size; i += 32) {
+            uint32_t p = rf_head + i;
+            if (p >= b) p -= b;
+            mi.id[i] = rf.id[p];
+            mi.sq[i] = rf.sq[p];
+            mi.aux[i] = rf.aux[p];
+        }
+        const uint32_t nf = rf_size;
+        for (uint32_t i = lane; i < rt_size; i += 32) {
+            uint32_t p = rt_head + i;
+            if (p >= b) p -= b;
+            mi.id[nf + i] = rt.id[p];
+            mi.sq[nf + i] = rt.sq[p];
+            mi.aux[nf + i] = rt.aux[p];
+        }
+        const uint32_t nm = nf + rt_size;
+        rf_head = rf_size = rt_head = rt_size = 0;
+        __syncwarp();
+        if (nm == 0) {
+            zmax_sq = zmax_dist = 0.0f;
+            return false;
+        }
+        rank_sort(mi, c.mo, nm, lane);
+        const uint32_t refill = min(nm, b);
+        for (uint32_t i = lane; i < nm; i += 32) {
+            if (i < refill) {
+                W.id[i] = c.mo.id[i];
+                W.sq[i] = c.mo.sq[i];
+                W.aux[i] = c.mo.aux[i];
+            } else {
+                const uint32_t p = i - refill;
+                rt.id[p] = c.mo.id[i];
+                rt.sq[p] = c.mo.sq[i];
+                rt.aux[p] = c.mo.aux[i];
+            }
+        }
+        wsize = refill;
+        rt_size = nm - refill;
+        __syncwarp();
+        recompute_zmax(lane);
+        return true;
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Exact squared distances for the rows named by lanes in `items` (lane j:
+// row id w). Results land in c.sqbuf[j], deg[w] in c.degbuf[j].
+// EXACT: the reference order (vecstore.cpp:77-95). All 32 lanes compute the
+//   squared differences of a 128-float chunk (coalesced float4 loads, one
+//   chunk of look-ahead) and scatter them transposed into smem; 4 lanes per
+//   row then run the four strided accumulator chains serially.
+// !EXACT: lane-parallel FMA partials + xor tree (within 1e-5 relative).
+// ---------------------------------------------------------------------------
+template <bool EXACT>
+__device__ void distances(const SearchLaunch& P, Common& c, uint32_t items, uint32_t w, int lane) {
     const IndexView& ix = P.ix;
     const uint32_t DS = ix.dstride, D = ix.padded, D4 = D & ~3u;
-    const int R = static_cast<int>(P.stage_rows);
     if ((items >> lane) & 1u) {
-        const float* row = ix.rows + static_cast<uint64_t>(w) * DS;
-        prefetch_l2_bulk(row, DS * 4u);
-        degbuf[lane] = __ldg(ix.deg + w);
+        prefetch_l2_bulk(ix.rows + static_cast<uint64_t>(w) * DS, DS * 4u);
+        c.degbuf[lane] = __ldg(ix.deg + w);
     }
+    constexpr int R = EXACT ? EXACT_ROWS : FAST_ROWS;
     uint32_t rest = items;
     while (rest) {
-        int jr[MAX_STAGE_ROWS];
-        const float* rp[MAX_STAGE_ROWS];
+        int jr[R];
+        const float* rp[R];
         int nb = 0;
 #pragma unroll
-        for (int r = 0; r < MAX_STAGE_ROWS; ++r) {
+        for (int r = 0; r < R; ++r) {
             jr[r] = 0;
-            if (r < R && rest) {
+            if (rest) {
                 jr[r] = __ffs(rest) - 1;
                 rest &= rest - 1;
                 nb = r + 1;
             }
-            uint32_t wr = __shfl_sync(FULL, w, jr[r]);
-            rp[r] = ix.rows + static_cast<uint64_t>(wr) * DS;
+            rp[r] = ix.rows + static_cast<uint64_t>(__shfl_sync(FULL, w, jr[r])) * DS;
         }
-        if (P.exact_dist) {
+        if (EXACT) {
             const int cr = lane >> 2, cc = lane & 3;
             float acc = 0.0f;
-            for (uint32_t base = 0; base < DS; base += 128) {
-                const uint32_t k = base + 4u * lane;
-                float4 qv = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (k < DS) qv = *reinterpret_cast<const float4*>(q + k);
+            float4 cur[R], nxt[R];
+            const uint32_t k0 = 4u * lane;
 #pragma unroll
-                for (int r = 0; r < MAX_STAGE_ROWS; ++r) {
+            for (int r = 0; r < R; ++r) {
+                cur[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (r < nb && k0 < DS) cur[r] = ldg_f4(rp[r] + k0);
+            }
+            for (uint32_t base = 0; base < DS; base += 128) {
+                const uint32_t k = base + 4u * lane, kn = k + 128;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    nxt[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (r < nb && kn < DS) nxt[r] = ldg_f4(rp[r] + kn);
+                }
+                float4 qv = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (k < DS) qv = *reinterpret_cast<const float4*>(c.q + k);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
                     if (r < nb) {
-                        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                        if (k < DS) v = ldg_f4(rp[r] + k);
-                        float d0 = __fsub_rn(v.x, qv.x), d1 = __fsub_rn(v.y, qv.y);
-                        float d2 = __fsub_rn(v.z, qv.z), d3 = __fsub_rn(v.w, qv.w);
-                        float4 p = make_float4(__fmul_rn(d0, d0), __fmul_rn(d1, d1),
-                                               __fmul_rn(d2, d2), __fmul_rn(d3, d3));
-                        *reinterpret_cast<float4*>(stage + r * STAGE_STRIDE + 4 * lane) = p;
+                        const float d0 = __fsub_rn(cur[r].x, qv.x), d1 = __fsub_rn(cur[r].y, qv.y);
+                        const float d2 = __fsub_rn(cur[r].z, qv.z), d3 = __fsub_rn(cur[r].w, qv.w);
+                        float* st = c.stage + (r * 4) * XSTR + lane;
+                        st[0] = __fmul_rn(d0, d0);
+                        st[XSTR] = __fmul_rn(d1, d1);
+                        st[2 * XSTR] = __fmul_rn(d2, d2);
+                        st[3 * XSTR] = __fmul_rn(d3, d3);
                     }
                 }
                 __syncwarp();
                 if (cr < nb) {
-                    const float* sp = stage + cr * STAGE_STRIDE + cc;
+                    const float* sp = c.stage + (cr * 4 + cc) * XSTR;
                     if (base + 128 <= D4) {
-#pragma unroll 8
-                        for (int t = 0; t < 32; ++t) acc = __fadd_rn(acc, sp[4 * t]);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const float4 x = *reinterpret_cast<const float4*>(sp + 4 * i);
+                            acc = __fadd_rn(acc, x.x);
+                            acc = __fadd_rn(acc, x.y);
+                            acc = __fadd_rn(acc, x.z);
+                            acc = __fadd_rn(acc, x.w);
+                        }
                     } else {
+                        const float* s0 = c.stage + (cr * 4) * XSTR;
                         for (int t = 0; t < 32; ++t) {
-                            uint32_t kk = base + 4u * t + cc;
+                            const uint32_t kk = base + 4u * t + cc;
                             if (kk < D4) {
-                                acc = __fadd_rn(acc, sp[4 * t]);
+                                acc = __fadd_rn(acc, sp[t]);
                             } else if (cc == 0 && kk < D) {
-                                // tail elements all go to acc0, in order
-                                acc = __fadd_rn(acc, sp[4 * t]);
-                                if (kk + 1 < D) acc = __fadd_rn(acc, sp[4 * t + 1]);
-                                if (kk + 2 < D) acc = __fadd_rn(acc, sp[4 * t + 2]);
+                                // tail elements all go to acc0, in order (vecstore.cpp:90-93)
+                                acc = __fadd_rn(acc, s0[t]);
+                                if (kk + 1 < D) acc = __fadd_rn(acc, s0[XSTR + t]);
+                                if (kk + 2 < D) acc = __fadd_rn(acc, s0[2 * XSTR + t]);
                             }
                         }
                     }
                 }
                 __syncwarp();
+#pragma unroll
+                for (int r = 0; r < R; ++r) cur[r] = nxt[r];
             }
-            float a1 = __shfl_down_sync(FULL, acc, 1);
-            float a2 = __shfl_down_sync(FULL, acc, 2);
-            float a3 = __shfl_down_sync(FULL, acc, 3);
+            const float a1 = __shfl_down_sync(FULL, acc, 1);
+            const float a2 = __shfl_down_sync(FULL, acc, 2);
+            const float a3 = __shfl_down_sync(FULL, acc, 3);
             int jmine = 0;
 #pragma unroll
-            for (int r = 0; r < MAX_STAGE_ROWS; ++r)
+            for (int r = 0; r < R; ++r)
                 if (r == cr) jmine = jr[r];
-            if (cc == 0 && cr < nb) sqbuf[jmine] = __fadd_rn(__fadd_rn(acc, a1), __fadd_rn(a2, a3));
+            if (cc == 0 && cr < nb) c.sqbuf[jmine] = __fadd_rn(__fadd_rn(acc, a1), __fadd_rn(a2, a3));
         } else {
-            float part[MAX_STAGE_ROWS];
+            float part[R];
 #pragma unroll
-            for (int r = 0; r < MAX_STAGE_ROWS; ++r) part[r] = 0.0f;
+            for (int r = 0; r < R; ++r) part[r] = 0.0f;
             for (uint32_t base = 0; base < DS; base += 128) {
                 const uint32_t k = base + 4u * lane;
                 if (k < DS) {
-                    float4 qv = *reinterpret_cast<const float4*>(q + k);
+                    const float4 qv = *reinterpret_cast<const float4*>(c.q + k);
 #pragma unroll
-                    for (int r = 0; r < MAX_STAGE_ROWS; ++r) {
+                    for (int r = 0; r < R; ++r) {
                         if (r < nb) {
-                            float4 v = ldg_f4(rp[r] + k);
-                            float d0 = v.x - qv.x, d1 = v.y - qv.y, d2 = v.z - qv.z, d3 = v.w - qv.w;
+                            const float4 v = ldg_f4(rp[r] + k);
+                            const float d0 = v.x - qv.x, d1 = v.y - qv.y, d2 = v.z - qv.z, d3 = v.w - qv.w;
                             part[r] = fmaf(d0, d0, part[r]);
                             part[r] = fmaf(d1, d1, part[r]);
                             part[r] = fmaf(d2, d2, part[r]);
@@ -479,12 +709,12 @@ __device__ void distances(const SearchLaunch& P, uint32_t items, uint32_t w, con
                 }
             }
 #pragma unroll
-            for (int r = 0; r < MAX_STAGE_ROWS; ++r) {
+            for (int r = 0; r < R; ++r) {
                 if (r < nb) {
                     float v = part[r];
 #pragma unroll
                     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-                    if (lane == 0) sqbuf[jr[r]] = v;
+                    if (lane == 0) c.sqbuf[jr[r]] = v;
                 }
             }
         }
@@ -501,8 +731,8 @@ __device__ float query_norm(const float* q, uint32_t D, int lane) {
         if (lane == 0)
             for (uint32_t k = D4; k < D; ++k) acc = __fadd_rn(acc, __fmul_rn(q[k], q[k]));
     }
-    float a1 = __shfl_sync(FULL, acc, 1), a2 = __shfl_sync(FULL, acc, 2),
-          a3 = __shfl_sync(FULL, acc, 3), a0 = __shfl_sync(FULL, acc, 0);
+    const float a1 = __shfl_sync(FULL, acc, 1), a2 = __shfl_sync(FULL, acc, 2),
+                a3 = __shfl_sync(FULL, acc, 3), a0 = __shfl_sync(FULL, acc, 0);
     return __fsqrt_rn(__fadd_rn(__fadd_rn(a0, a1), __fadd_rn(a2, a3)));
 }
 
@@ -522,26 +752,45 @@ __device__ __forceinline__ float code_sum(const float* T, uint32_t L, uint32_t m
         }
     } else {
         for (uint32_t l = 0; l < L; ++l) {
-            uint32_t word = __ldg(cw_global + (l >> 3));
+            const uint32_t word = __ldg(cw_global + (l >> 3));
             sum = __fadd_rn(sum, T[l * m + ((word >> (4 * (l & 7))) & 15u)]);
         }
     }
     return sum;
 }
 
+__device__ __forceinline__ void prefetch_block(const IndexView& ix, uint32_t u, uint32_t deg) {
+    if (deg == 0) return;
+    const uint8_t* blk = ix.adj + static_cast<uint64_t>(u) * ix.block_bytes;
+    const uint32_t S = ix.slot_stride;
+    const uint32_t b4 = (4u * deg + 15u) & ~15u;
+    prefetch_l2_bulk(blk, b4);
+    prefetch_l2_bulk(blk + 4u * S, b4);
+    prefetch_l2_bulk(blk + 8u * S, b4);
+    prefetch_l2_bulk(blk + 12u * S, b4);
+    prefetch_l2_bulk(blk + 16u * S, 4u * ix.cwp * deg);
+}
+
 // routing.cpp:139-204 for W slot `slot`
-__device__ void expand(const SearchLaunch& P, Tfb& s, uint32_t slot, const float* q,
-                       const float* T, float* stage, float* sqbuf, uint32_t* degbuf, int lane) {
+template <class TFB, bool EXACT>
+__device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, int lane) {
     const IndexView& ix = P.ix;
     const float TAU_HI = 1.0f + 1e-6f;
-    const uint32_t u = s.W.id[slot];
-    const float usq = s.W.sq[slot];
-    const uint32_t deg = s.W.aux[slot] & ~VISITED;
-    __syncwarp();
-    if (lane == 0) s.W.aux[slot] = deg | VISITED;
-    __syncwarp();
-    ++s.n_visited;
-    s.n_edges += deg;
+    uint32_t u, deg;
+    float usq;
+    s.entry(slot, u, usq, deg);
+    s.set_visited(slot, lane);
+    // speculative L2 prefetch of the node expanded next if nothing nearer is
+    // admitted meanwhile (adjacency is the head of the next dependency chain)
+    {
+        const uint32_t nx = s.next_unvisited(lane);
+        if (nx != EMPTY) {
+            const uint32_t nid = s.entry_id(nx), ndeg = s.entry_deg(nx);
+            if (lane == 0) prefetch_block(ix, nid, ndeg);
+        }
+    }
+    ++c.n_visited;
+    c.n_edges += deg;
     const float duq = __fsqrt_rn(usq);
     const bool exact_mode = (duq == 0.0f) || !P.use_prt;
     const uint8_t* blk = ix.adj + static_cast<uint64_t>(u) * ix.block_bytes;
@@ -566,20 +815,20 @@ __device__ void expand(const SearchLaunch& P, Tfb& s, uint32_t slot, const float
             bo = __ldg(bo_a + j);
             const uint32_t* cp = cw_a + static_cast<uint64_t>(j) * ix.cwp;
             if (ix.cwp == 4) {
-                uint4 v = __ldg(reinterpret_cast<const uint4*>(cp));
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(cp));
                 cw[0] = v.x; cw[1] = v.y; cw[2] = v.z; cw[3] = v.w;
             } else if (ix.cwp == 2) {
-                uint2 v = __ldg(reinterpret_cast<const uint2*>(cp));
+                const uint2 v = __ldg(reinterpret_cast<const uint2*>(cp));
                 cw[0] = v.x; cw[1] = v.y;
             } else if (ix.cwp == 1) {
                 cw[0] = __ldg(cp);
             }
         }
-        const bool cand = active && !marked(s, w);
+        const bool cand = active && !marked(c, w);
         const uint32_t cand_mask = __ballot_sync(FULL, cand);
         // duplicate targets inside the group (reference order: a later copy
         // is skipped when an earlier copy passed and marked it)
-        unsigned long long key =
+        const unsigned long long key =
             cand ? static_cast<unsigned long long>(w) : ((1ull << 32) | static_cast<unsigned>(lane));
         const uint32_t same = __match_any_sync(FULL, key) & cand_mask;
 
@@ -591,10 +840,10 @@ __device__ void expand(const SearchLaunch& P, Tfb& s, uint32_t slot, const float
             if (exact_mode) {
                 spec = true;
             } else {
-                float tau = prt_threshold(en, duq, adist0);
+                const float tau = prt_threshold(en, duq, adist0);
                 if (tau < TAU_HI) {
                     const uint32_t* cp = cw_a + static_cast<uint64_t>(j) * ix.cwp;
-                    float sum = code_sum(T, ix.L, ix.m, cp, ix.cwp, cw);
+                    const float sum = code_sum(c.T, ix.L, ix.m, cp, ix.cwp, cw);
                     quot = __fdiv_rn(__fdiv_rn(__fsub_rn(sum, bo), duq), cbeta);
                     spec = (tau <= -1.0f) || (quot >= tau);
                 }
@@ -602,7 +851,7 @@ __device__ void expand(const SearchLaunch& P, Tfb& s, uint32_t slot, const float
         }
         // (ii) compaction, (iii) exact distances of survivors
         const uint32_t surv = __ballot_sync(FULL, spec);
-        if (surv) distances(P, surv, w, q, stage, sqbuf, degbuf, lane);
+        if (surv) distances<EXACT>(P, c, surv, w, lane);
 
         // (iv) in-order replay with the live radius
         uint32_t passed = 0;
@@ -617,7 +866,7 @@ __device__ void expand(const SearchLaunch& P, Tfb& s, uint32_t slot, const float
             const uint32_t w_j = __shfl_sync(FULL, w, jl);
             bool pass = true;
             if (!exact_mode) {
-                float tau = prt_threshold(en_j, duq, s.admission_dist());
+                const float tau = prt_threshold(en_j, duq, s.admission_dist());
                 if (tau >= TAU_HI)
                     pass = false;
                 else if (tau <= -1.0f)
@@ -627,26 +876,24 @@ __device__ void expand(const SearchLaunch& P, Tfb& s, uint32_t slot, const float
             }
             if (!pass) continue;
             passed |= 1u << jl;
-            ++s.n_pass;
-            ++s.n_exact;
-            const float sq_j = sqbuf[jl];
-            const uint32_t deg_j = degbuf[jl];
-            __syncwarp();
-            mark(s, w_j, lane);
-            if (sq_j < s.admission_sq()) {
-                admit(s, w_j, sq_j, deg_j, lane);
-            } else {
-                ring_push(s.rf, s.b, s.rf_head, s.rf_size, w_j, sq_j, deg_j, lane);
-                __syncwarp();
-            }
+            ++c.n_pass;
+            ++c.n_exact;
+            const float sq_j = c.sqbuf[jl];
+            const uint32_t deg_j = c.degbuf[jl];
+            mark(c, w_j, lane);
+            if (sq_j < s.admission_sq())
+                s.admit(w_j, sq_j, deg_j, lane);
+            else
+                s.push_fp(w_j, sq_j, deg_j, lane);
         }
         const bool not_test = cand && ((same & lt & passed) != 0u);
-        s.n_test += __popc(cand_mask) - __popc(__ballot_sync(FULL, not_test));
+        c.n_test += __popc(cand_mask) - __popc(__ballot_sync(FULL, not_test));
         __syncwarp();
     }
 }
 
-__global__ void __launch_bounds__(128) pag_search_kernel(const __grid_constant__ SearchLaunch P) {
+template <class TFB, bool EXACT>
+__global__ void __launch_bounds__(128, 4) pag_search_kernel(const __grid_constant__ SearchLaunch P) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -655,31 +902,27 @@ __global__ void __launch_bounds__(128) pag_search_kernel(const __grid_constant__
     uint8_t* gw = P.gscratch + static_cast<uint64_t>(slot) * P.gscratch_stride;
     const IndexView& ix = P.ix;
 
-    float* q = reinterpret_cast<float*>(sw + P.off_q);
-    float* T = reinterpret_cast<float*>(sw + P.off_T);
-    float* sqbuf = reinterpret_cast<float*>(sw + P.off_sqbuf);
-    uint32_t* degbuf = reinterpret_cast<uint32_t*>(sw + P.off_sqbuf + 128);
-    float* stage = reinterpret_cast<float*>(sw + P.off_stage);
-
-    Tfb s;
-    s.b = P.b;
-    s.cap_r = P.efS;
-    s.W = make_arr((P.W_in_smem ? sw : gw) + P.off_W, P.b);
-    s.rf = make_arr((P.rings_in_smem ? sw : gw) + P.off_rf, P.b);
-    s.rt = make_arr((P.rings_in_smem ? sw : gw) + P.off_rt, P.b);
+    Common c;
+    c.q = reinterpret_cast<float*>(sw + P.off_q);
+    c.T = reinterpret_cast<float*>(sw + P.off_T);
+    c.sqbuf = reinterpret_cast<float*>(sw + P.off_sqbuf);
+    c.degbuf = reinterpret_cast<uint32_t*>(sw + P.off_sqbuf + 128);
+    c.stage = reinterpret_cast<float*>(sw + P.off_stage);
     {
         uint8_t* rl = (P.rl_in_smem ? sw : gw) + P.off_rl;
         const uint32_t cap = P.efS ? P.efS : 1;
-        s.rlA = make_arr(rl, cap);
-        s.rlB = make_arr(rl + 12ull * cap, cap);
+        c.rlA = make_arr(rl, cap);
+        c.rlB = make_arr(rl + 12ull * cap, cap);
         uint8_t* mg = (P.merge_in_smem ? sw : gw) + P.off_merge;
-        s.mi = make_arr(mg, 2 * P.b);
-        s.mo = make_arr(mg + 24ull * P.b, 2 * P.b);
+        c.mo = make_arr(mg + 24ull * P.b, 2 * P.b);
     }
-    s.hs = reinterpret_cast<uint32_t*>(sw + P.off_hash);
-    s.hs_log2 = P.hash_log2;
-    s.gt = P.gtab + (static_cast<uint64_t>(slot) << P.gtab_log2);
-    s.gt_log2 = P.gtab_log2;
+    c.cap_r = P.efS;
+    c.hs = reinterpret_cast<uint32_t*>(sw + P.off_hash);
+    c.hs_log2 = P.hash_log2;
+    c.gt = P.gtab + (static_cast<uint64_t>(slot) << P.gtab_log2);
+    c.gt_log2 = P.gtab_log2;
+    TFB s;
+    s.init(P.b, sw, gw, P);
     uint32_t epoch = P.slot_epoch[slot];
 
     while (true) {
@@ -691,35 +934,32 @@ __global__ void __launch_bounds__(128) pag_search_kernel(const __grid_constant__
 
         // ---- reset (routing.cpp:12-30)
         if (++epoch == 0) {  // epoch wrap: clear this slot's table
-            for (uint32_t i = lane; i < (1u << s.gt_log2); i += 32) s.gt[i] = 0;
+            for (uint32_t i = lane; i < (1u << c.gt_log2); i += 32) c.gt[i] = 0;
             epoch = 1;
         }
-        s.epoch = epoch;
-        s.wsize = 0;
-        s.zmax_sq = s.zmax_dist = 0.0f;
-        s.zmax_idx = 0;
-        s.rf_head = s.rf_size = s.rt_head = s.rt_size = 0;
-        s.rl_cur = 0;
-        s.rl_size = 0;
-        s.hs_count = 0;
-        s.gt_count = 0;
-        s.gt_used = false;
-        s.overflow = false;
-        s.n_exact = s.n_test = s.n_pass = s.n_visited = s.n_edges = 0;
-        for (uint32_t i = lane; i < (1u << s.hs_log2); i += 32) s.hs[i] = EMPTY;
+        c.epoch = epoch;
+        c.rl_cur = 0;
+        c.rl_size = 0;
+        c.hs_count = 0;
+        c.gt_count = 0;
+        c.gt_used = false;
+        c.overflow = false;
+        c.n_exact = c.n_test = c.n_pass = c.n_visited = c.n_edges = 0;
+        s.reset();
+        for (uint32_t i = lane; i < (1u << c.hs_log2); i += 32) c.hs[i] = EMPTY;
 
         // ---- query prep (routing.cpp:253-259): pad, cosine-normalise
         const float* qraw = P.queries + static_cast<uint64_t>(qid) * ix.dim;
-        for (uint32_t k = lane; k < ix.dstride; k += 32) q[k] = (k < ix.dim) ? __ldg(qraw + k) : 0.0f;
+        for (uint32_t k = lane; k < ix.dstride; k += 32) c.q[k] = (k < ix.dim) ? __ldg(qraw + k) : 0.0f;
         __syncwarp();
         uint32_t status = 0;
         if (ix.cosine) {
-            const float nrm = query_norm(q, ix.padded, lane);
+            const float nrm = query_norm(c.q, ix.padded, lane);
             if (nrm == 0.0f) {
                 status |= kStatusZeroCosineQuery;
             } else {
                 __syncwarp();
-                for (uint32_t k = lane; k < ix.padded; k += 32) q[k] = __fdiv_rn(q[k], nrm);
+                for (uint32_t k = lane; k < ix.padded; k += 32) c.q[k] = __fdiv_rn(c.q[k], nrm);
             }
             __syncwarp();
         }
@@ -733,61 +973,89 @@ __global__ void __launch_bounds__(128) pag_search_kernel(const __grid_constant__
             continue;
         }
 
+        // ---- seeds (routing.cpp:219-227): first <= b unmarked valid entries.
+        // Their rows are requested before the table is built so the two overlap.
+        uint32_t seed_sel[2] = {0, 0}, seed_id[2] = {0, 0};
+        {
+            uint32_t room = P.b;
+            for (uint32_t e0 = 0, g = 0; e0 < ix.n_entries && room && g < 2; e0 += 32, ++g) {
+                for (uint32_t t = 0; t < 32 && e0 + t < ix.n_entries && room; ++t) {
+                    const uint32_t id = __ldg(ix.entries + e0 + t);
+                    if (static_cast<uint64_t>(id) >= ix.n) continue;
+                    if (marked(c, id)) continue;
+                    mark(c, id, lane);
+                    if (lane == static_cast<int>(t)) seed_id[g] = id;
+                    seed_sel[g] |= 1u << t;
+                    --room;
+                }
+            }
+            if ((seed_sel[0] >> lane) & 1u)
+                prefetch_l2_bulk(ix.rows + static_cast<uint64_t>(seed_id[0]) * ix.dstride, ix.dstride * 4u);
+        }
+
         // ---- projection table (projection.cpp:123-137), serial dot per entry
         {
             const uint32_t Lm = ix.L * ix.m, sub = ix.sub_dim, m = ix.m;
             for (uint32_t e = lane; e < Lm; e += 32) {
                 const uint32_t l = e / m, jj = e - l * m;
-                const float* xl = q + l * sub;
+                const float* xl = c.q + l * sub;
                 const float* rT = ix.refsT + static_cast<uint64_t>(l) * sub * m + jj;
                 float dot = 0.0f;
-                for (uint32_t c = 0; c < sub; ++c) dot = __fadd_rn(dot, __fmul_rn(xl[c], __ldg(rT + c * m)));
-                T[e] = dot;
+                for (uint32_t cc = 0; cc < sub; ++cc) dot = __fadd_rn(dot, __fmul_rn(xl[cc], __ldg(rT + cc * m)));
+                c.T[e] = dot;
             }
         }
         __syncwarp();
 
-        // ---- seeds (routing.cpp:219-227): first <= b unmarked valid entries
-        for (uint32_t e0 = 0; e0 < ix.n_entries && s.wsize < s.b; e0 += 32) {
-            // sequential selection (duplicates / out-of-range skipped)
-            uint32_t sel = 0, myid = 0;
-            uint32_t room = s.b - s.wsize;
+        for (int g = 0; g < 2; ++g) {
+            if (!seed_sel[g]) continue;
+            distances<EXACT>(P, c, seed_sel[g], seed_id[g], lane);
+            uint32_t rem = seed_sel[g];
+            while (rem) {
+                const int t = __ffs(rem) - 1;
+                rem &= rem - 1;
+                const uint32_t id = __shfl_sync(FULL, seed_id[g], t);
+                ++c.n_exact;
+                s.append(id, c.sqbuf[t], c.degbuf[t], lane);
+            }
+            __syncwarp();
+        }
+        // entry lists longer than 64 (b > 64 and n_entries > 64): remaining seeds
+        for (uint32_t e0 = 64; e0 < ix.n_entries && s.wsize < P.b && !c.overflow; e0 += 32) {
+            uint32_t sel = 0, myid = 0, room = P.b - s.wsize;
             for (uint32_t t = 0; t < 32 && e0 + t < ix.n_entries && room; ++t) {
                 const uint32_t id = __ldg(ix.entries + e0 + t);
                 if (static_cast<uint64_t>(id) >= ix.n) continue;
-                if (marked(s, id)) continue;
-                mark(s, id, lane);
+                if (marked(c, id)) continue;
+                mark(c, id, lane);
                 if (lane == static_cast<int>(t)) myid = id;
                 sel |= 1u << t;
                 --room;
             }
-            if (s.overflow) break;
-            distances(P, sel, myid, q, stage, sqbuf, degbuf, lane);
+            distances<EXACT>(P, c, sel, myid, lane);
             uint32_t rem = sel;
             while (rem) {
                 const int t = __ffs(rem) - 1;
                 rem &= rem - 1;
-                const uint32_t id = __shfl_sync(FULL, myid, t);
-                ++s.n_exact;
-                w_append(s, id, sqbuf[t], degbuf[t], lane);
-                __syncwarp();
+                ++c.n_exact;
+                s.append(__shfl_sync(FULL, myid, t), c.sqbuf[t], c.degbuf[t], lane);
             }
             __syncwarp();
         }
 
         // ---- rounds (routing.cpp:229-240)
-        for (uint32_t r = 0; r < P.r_max && !s.overflow; ++r) {
-            while (!s.overflow) {
-                const uint32_t i = next_unvisited(s, lane);
+        for (uint32_t r = 0; r < P.r_max && !c.overflow; ++r) {
+            while (!c.overflow) {
+                const uint32_t i = s.next_unvisited(lane);
                 if (i == EMPTY) break;
-                expand(P, s, i, q, T, stage, sqbuf, degbuf, lane);
+                expand<TFB, EXACT>(P, c, s, i, lane);
             }
-            if (r + 1 == P.r_max || !end_round(s, lane)) break;
+            if (r + 1 == P.r_max || !s.end_round(c, lane)) break;
         }
         // final flush (routing.cpp:242) and truncation to K (:244-246)
-        flush_working(s, lane);
-        const uint32_t k_out = min(P.K, s.rl_size);
-        const Arr res = s.rl_cur_arr();
+        s.flush(c, lane);
+        const uint32_t k_out = min(P.K, c.rl_size);
+        const Arr res = c.rl_cur_arr();
         for (uint32_t i = lane; i < k_out; i += 32) {
             P.out_ids[static_cast<uint64_t>(qid) * P.K + i] = res.id[i];
             P.out_sq[static_cast<uint64_t>(qid) * P.K + i] = res.sq[i];
@@ -795,18 +1063,36 @@ __global__ void __launch_bounds__(128) pag_search_kernel(const __grid_constant__
         if (lane == 0) {
             P.out_n[qid] = k_out;
             uint32_t* st = P.out_stats + static_cast<uint64_t>(qid) * kStatWords;
-            st[kStatExact] = s.n_exact;
-            st[kStatTest] = s.n_test;
-            st[kStatPass] = s.n_pass;
-            st[kStatVisited] = s.n_visited;
-            st[kStatEdges] = s.n_edges;
-            st[kStatStatus] = s.overflow ? kStatusVisitedOverflow : 0u;
-            st[6] = s.hs_count + s.gt_count;  // marks held
+            st[kStatExact] = c.n_exact;
+            st[kStatTest] = c.n_test;
+            st[kStatPass] = c.n_pass;
+            st[kStatVisited] = c.n_visited;
+            st[kStatEdges] = c.n_edges;
+            st[kStatStatus] = c.overflow ? kStatusVisitedOverflow : 0u;
+            st[6] = c.hs_count + c.gt_count;  // marks held
             st[7] = 0;
         }
         __syncwarp();
     }
     if (lane == 0) P.slot_epoch[slot] = epoch;
+}
+
+template <class TFB, bool EXACT>
+cudaError_t launch_t(const SearchLaunch& L, int grid, size_t smem, cudaStream_t stream) {
+    cudaError_t e = cudaFuncSetAttribute(pag_search_kernel<TFB, EXACT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    pag_search_kernel<TFB, EXACT><<<grid, L.warps_per_block * 32, smem, stream>>>(L);
+    return cudaGetLastError();
+}
+
+template <class TFB, bool EXACT>
+cudaError_t occupancy_t(int warps_per_block, size_t smem, int* bps) {
+    cudaError_t e = cudaFuncSetAttribute(pag_search_kernel<TFB, EXACT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, pag_search_kernel<TFB, EXACT>,
+                                                         warps_per_block * 32, smem);
 }
 
 }  // namespace
@@ -815,21 +1101,25 @@ size_t search_kernel_smem(const SearchLaunch& L) {
     return static_cast<size_t>(L.warp_smem_bytes) * L.warps_per_block;
 }
 
-cudaError_t search_occupancy(int warps_per_block, size_t smem_bytes, int* blocks_per_sm) {
-    cudaError_t e = cudaFuncSetAttribute(pag_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem_bytes));
-    if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, pag_search_kernel,
-                                                         warps_per_block * 32, smem_bytes);
+bool search_uses_registers(const SearchLaunch& L) { return L.b <= 32; }
+
+cudaError_t search_occupancy(const SearchLaunch& L, int* blocks_per_sm) {
+    const size_t smem = search_kernel_smem(L);
+    const int wpb = static_cast<int>(L.warps_per_block);
+    if (search_uses_registers(L))
+        return L.exact_dist ? occupancy_t<TfbReg, true>(wpb, smem, blocks_per_sm)
+                            : occupancy_t<TfbReg, false>(wpb, smem, blocks_per_sm);
+    return L.exact_dist ? occupancy_t<TfbMem, true>(wpb, smem, blocks_per_sm)
+                        : occupancy_t<TfbMem, false>(wpb, smem, blocks_per_sm);
 }
 
 cudaError_t launch_search(const SearchLaunch& L, int grid, cudaStream_t stream) {
     const size_t smem = search_kernel_smem(L);
-    cudaError_t e = cudaFuncSetAttribute(pag_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    pag_search_kernel<<<grid, L.warps_per_block * 32, smem, stream>>>(L);
-    return cudaGetLastError();
+    if (search_uses_registers(L))
+        return L.exact_dist ? launch_t<TfbReg, true>(L, grid, smem, stream)
+                            : launch_t<TfbReg, false>(L, grid, smem, stream);
+    return L.exact_dist ? launch_t<TfbMem, true>(L, grid, smem, stream)
+                        : launch_t<TfbMem, false>(L, grid, smem, stream);
 }
 
 }  // namespace pagdev

@@ -1,0 +1,8 @@
+set -x
+python -m pytest tests -x -q -m gpu 2>&1 | tail -25
+python bench.py --steps 20 --warmup 5 > gpurun_out/bench2.json 2> gpurun_out/bench2.err; echo bench_rc=$?
+tail -3 gpurun_out/bench2.err
+P="python bench.py --efs 70 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
+$P > gpurun_out/prof_plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $P > gpurun_out/ncu1.log 2>&1; echo ncu1=$?
+ncu --set full --clock-control none --import-source on -k regex:pag_search -s 2 -c 1 -o gpurun_out/prof_search $P > gpurun_out/ncu2.log 2>&1; echo ncu2=$?
