@@ -503,7 +503,7 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     L.off_q = off;
     off = align16(off + 4 * ix.dstride);
     L.off_T = off;
-    off = align16(off + 4 * ix.L * ix.m);
+    off = align16(off + 4 * ix.L * 16);  // T rows padded to 16 (m <= 16)
     L.off_hash = off;
     off = align16(off + (4u << L.hash_log2));
     L.off_sqbuf = off;

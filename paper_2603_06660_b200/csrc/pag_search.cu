@@ -589,136 +589,180 @@ struct TfbMem {
 // row id w). Results land in c.sqbuf[j], deg[w] in c.degbuf[j].
 // EXACT: the reference order (vecstore.cpp:77-95). All 32 lanes compute the
 //   squared differences of a 128-float chunk (coalesced float4 loads, one
-//   chunk of look-ahead) and scatter them transposed into smem; 4 lanes per
-//   row then run the four strided accumulator chains serially.
-// !EXACT: lane-parallel FMA partials + xor tree (within 1e-5 relative).
+//   chunk of look-ahead, packed f32x2 arithmetic) and scatter them transposed
+//   into smem; 4 lanes per row then run the four strided accumulator chains
+//   serially (8 x LDS.128 + 32 FADD per chunk).
+// !EXACT: lane-parallel packed-FMA partials + xor tree (within 1e-5 rel).
+// NCH > 0: padded_dim == dstride == 128 * NCH (compile-time chunk count);
+// NCH == 0: any padded_dim (bounds checks, reference tail handling).
 // ---------------------------------------------------------------------------
-template <bool EXACT>
-__device__ void distances(const SearchLaunch& P, Common& c, uint32_t items, uint32_t w, int lane) {
-    const IndexView& ix = P.ix;
-    const uint32_t DS = ix.dstride, D = ix.padded, D4 = D & ~3u;
-    if ((items >> lane) & 1u) {
-        prefetch_l2_bulk(ix.rows + static_cast<uint64_t>(w) * DS, DS * 4u);
-        c.degbuf[lane] = __ldg(ix.deg + w);
+__device__ __forceinline__ float2 sq2(float2 v, float2 q) {  // (v - q)^2 per component, no contraction
+    const float2 d = __fadd2_rn(v, make_float2(-q.x, -q.y));
+    return __fmul2_rn(d, d);
+}
+
+__device__ __forceinline__ int take_batch(uint32_t& rest, int (&jr)[4]) {
+    int nb = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        jr[r] = 0;
+        if (rest) {
+            jr[r] = __ffs(rest) - 1;
+            rest &= rest - 1;
+            nb = r + 1;
+        }
     }
-    constexpr int R = EXACT ? EXACT_ROWS : FAST_ROWS;
+    return nb;
+}
+
+template <int NCH>
+__device__ void dist_exact(const SearchLaunch& P, Common& c, uint32_t items, uint32_t w, int lane) {
+    const IndexView& ix = P.ix;
+    const uint32_t DS = NCH ? 128u * NCH : ix.dstride;
+    const uint32_t D = NCH ? DS : ix.padded, D4 = D & ~3u;
+    const uint32_t nch = NCH ? NCH : (DS + 127u) / 128u;
+    const int cr = lane >> 2, cc = lane & 3;
     uint32_t rest = items;
     while (rest) {
-        int jr[R];
-        const float* rp[R];
-        int nb = 0;
+        int jr[4];
+        const int nb = take_batch(rest, jr);
+        const float* rp[4];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            jr[r] = 0;
-            if (rest) {
-                jr[r] = __ffs(rest) - 1;
-                rest &= rest - 1;
-                nb = r + 1;
-            }
-            rp[r] = ix.rows + static_cast<uint64_t>(__shfl_sync(FULL, w, jr[r])) * DS;
+        for (int r = 0; r < 4; ++r) {
+            // rows past nb alias row 0 (L1 hits), so loads need no predicate
+            const uint32_t wr = __shfl_sync(FULL, w, r < nb ? jr[r] : jr[0]);
+            rp[r] = ix.rows + static_cast<uint64_t>(wr) * DS + 4u * lane;
         }
-        if (EXACT) {
-            const int cr = lane >> 2, cc = lane & 3;
-            float acc = 0.0f;
-            float4 cur[R], nxt[R];
-            const uint32_t k0 = 4u * lane;
+        float acc = 0.0f;
+        float4 cur[4], nxt[4];
+        const bool in0 = NCH || 4u * lane < DS;
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                cur[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (r < nb && k0 < DS) cur[r] = ldg_f4(rp[r] + k0);
-            }
-            for (uint32_t base = 0; base < DS; base += 128) {
-                const uint32_t k = base + 4u * lane, kn = k + 128;
+        for (int r = 0; r < 4; ++r) cur[r] = in0 ? ldg_f4(rp[r]) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll(NCH ? NCH : 1)
+        for (uint32_t ch = 0; ch < nch; ++ch) {
+            const uint32_t base = 128u * ch;
+            const uint32_t kn = base + 128u + 4u * lane;
+            const bool inn = NCH ? (ch + 1 < nch) : (kn < DS);
 #pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    nxt[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (r < nb && kn < DS) nxt[r] = ldg_f4(rp[r] + kn);
-                }
-                float4 qv = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (k < DS) qv = *reinterpret_cast<const float4*>(c.q + k);
+            for (int r = 0; r < 4; ++r)
+                nxt[r] = inn ? ldg_f4(rp[r] + base + 128u) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const bool in = NCH || base + 4u * lane < DS;
+            const float4 qv = in ? *reinterpret_cast<const float4*>(c.q + base + 4u * lane)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+            float* st = c.stage + lane;
 #pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    if (r < nb) {
-                        const float d0 = __fsub_rn(cur[r].x, qv.x), d1 = __fsub_rn(cur[r].y, qv.y);
-                        const float d2 = __fsub_rn(cur[r].z, qv.z), d3 = __fsub_rn(cur[r].w, qv.w);
-                        float* st = c.stage + (r * 4) * XSTR + lane;
-                        st[0] = __fmul_rn(d0, d0);
-                        st[XSTR] = __fmul_rn(d1, d1);
-                        st[2 * XSTR] = __fmul_rn(d2, d2);
-                        st[3 * XSTR] = __fmul_rn(d3, d3);
-                    }
-                }
-                __syncwarp();
-                if (cr < nb) {
-                    const float* sp = c.stage + (cr * 4 + cc) * XSTR;
-                    if (base + 128 <= D4) {
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            const float4 x = *reinterpret_cast<const float4*>(sp + 4 * i);
-                            acc = __fadd_rn(acc, x.x);
-                            acc = __fadd_rn(acc, x.y);
-                            acc = __fadd_rn(acc, x.z);
-                            acc = __fadd_rn(acc, x.w);
-                        }
-                    } else {
-                        const float* s0 = c.stage + (cr * 4) * XSTR;
-                        for (int t = 0; t < 32; ++t) {
-                            const uint32_t kk = base + 4u * t + cc;
-                            if (kk < D4) {
-                                acc = __fadd_rn(acc, sp[t]);
-                            } else if (cc == 0 && kk < D) {
-                                // tail elements all go to acc0, in order (vecstore.cpp:90-93)
-                                acc = __fadd_rn(acc, s0[t]);
-                                if (kk + 1 < D) acc = __fadd_rn(acc, s0[XSTR + t]);
-                                if (kk + 2 < D) acc = __fadd_rn(acc, s0[2 * XSTR + t]);
-                            }
-                        }
-                    }
-                }
-                __syncwarp();
-#pragma unroll
-                for (int r = 0; r < R; ++r) cur[r] = nxt[r];
-            }
-            const float a1 = __shfl_down_sync(FULL, acc, 1);
-            const float a2 = __shfl_down_sync(FULL, acc, 2);
-            const float a3 = __shfl_down_sync(FULL, acc, 3);
-            int jmine = 0;
-#pragma unroll
-            for (int r = 0; r < R; ++r)
-                if (r == cr) jmine = jr[r];
-            if (cc == 0 && cr < nb) c.sqbuf[jmine] = __fadd_rn(__fadd_rn(acc, a1), __fadd_rn(a2, a3));
-        } else {
-            float part[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) part[r] = 0.0f;
-            for (uint32_t base = 0; base < DS; base += 128) {
-                const uint32_t k = base + 4u * lane;
-                if (k < DS) {
-                    const float4 qv = *reinterpret_cast<const float4*>(c.q + k);
-#pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        if (r < nb) {
-                            const float4 v = ldg_f4(rp[r] + k);
-                            const float d0 = v.x - qv.x, d1 = v.y - qv.y, d2 = v.z - qv.z, d3 = v.w - qv.w;
-                            part[r] = fmaf(d0, d0, part[r]);
-                            part[r] = fmaf(d1, d1, part[r]);
-                            part[r] = fmaf(d2, d2, part[r]);
-                            part[r] = fmaf(d3, d3, part[r]);
-                        }
-                    }
-                }
-            }
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
+            for (int r = 0; r < 4; ++r) {
                 if (r < nb) {
-                    float v = part[r];
-#pragma unroll
-                    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-                    if (lane == 0) c.sqbuf[jr[r]] = v;
+                    const float2 lo = sq2(make_float2(cur[r].x, cur[r].y), make_float2(qv.x, qv.y));
+                    const float2 hi = sq2(make_float2(cur[r].z, cur[r].w), make_float2(qv.z, qv.w));
+                    st[(r * 4 + 0) * XSTR] = lo.x;
+                    st[(r * 4 + 1) * XSTR] = lo.y;
+                    st[(r * 4 + 2) * XSTR] = hi.x;
+                    st[(r * 4 + 3) * XSTR] = hi.y;
                 }
+            }
+            __syncwarp();
+            if (cr < nb) {
+                const float* sp = c.stage + (cr * 4 + cc) * XSTR;
+                if (NCH || base + 128 <= D4) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const float4 x = *reinterpret_cast<const float4*>(sp + 4 * i);
+                        acc = __fadd_rn(acc, x.x);
+                        acc = __fadd_rn(acc, x.y);
+                        acc = __fadd_rn(acc, x.z);
+                        acc = __fadd_rn(acc, x.w);
+                    }
+                } else {
+                    const float* s0 = c.stage + (cr * 4) * XSTR;
+                    for (int t = 0; t < 32; ++t) {
+                        const uint32_t kk = base + 4u * t + cc;
+                        if (kk < D4) {
+                            acc = __fadd_rn(acc, sp[t]);
+                        } else if (cc == 0 && kk < D) {
+                            // tail elements all go to acc0, in order (vecstore.cpp:90-93)
+                            acc = __fadd_rn(acc, s0[t]);
+                            if (kk + 1 < D) acc = __fadd_rn(acc, s0[XSTR + t]);
+                            if (kk + 2 < D) acc = __fadd_rn(acc, s0[2 * XSTR + t]);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < 4; ++r) cur[r] = nxt[r];
+        }
+        const float a1 = __shfl_down_sync(FULL, acc, 1);
+        const float a2 = __shfl_down_sync(FULL, acc, 2);
+        const float a3 = __shfl_down_sync(FULL, acc, 3);
+        int jmine = jr[0];
+#pragma unroll
+        for (int r = 1; r < 4; ++r)
+            if (r == cr) jmine = jr[r];
+        if (cc == 0 && cr < nb) c.sqbuf[jmine] = __fadd_rn(__fadd_rn(acc, a1), __fadd_rn(a2, a3));
+    }
+}
+
+template <int NCH>
+__device__ void dist_fast(const SearchLaunch& P, Common& c, uint32_t items, uint32_t w, int lane) {
+    const IndexView& ix = P.ix;
+    const uint32_t DS = NCH ? 128u * NCH : ix.dstride;
+    const uint32_t nch = NCH ? NCH : (DS + 127u) / 128u;
+    uint32_t rest = items;
+    while (rest) {
+        int jr[4];
+        const int nb = take_batch(rest, jr);
+        const float* rp[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uint32_t wr = __shfl_sync(FULL, w, r < nb ? jr[r] : jr[0]);
+            rp[r] = ix.rows + static_cast<uint64_t>(wr) * DS + 4u * lane;
+        }
+        float2 part[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) part[r] = make_float2(0.f, 0.f);
+#pragma unroll 2
+        for (uint32_t ch = 0; ch < nch; ++ch) {
+            const uint32_t base = 128u * ch;
+            if (NCH || base + 4u * lane < DS) {
+                const float4 qv = *reinterpret_cast<const float4*>(c.q + base + 4u * lane);
+                const float2 nqlo = make_float2(-qv.x, -qv.y), nqhi = make_float2(-qv.z, -qv.w);
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    if (r < nb) {
+                        const float4 v = ldg_f4(rp[r] + base);
+                        const float2 dlo = __fadd2_rn(make_float2(v.x, v.y), nqlo);
+                        const float2 dhi = __fadd2_rn(make_float2(v.z, v.w), nqhi);
+                        part[r] = __ffma2_rn(dlo, dlo, part[r]);
+                        part[r] = __ffma2_rn(dhi, dhi, part[r]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (r < nb) {
+                float v = part[r].x + part[r].y;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+                if (lane == 0) c.sqbuf[jr[r]] = v;
             }
         }
     }
+}
+
+template <bool EXACT, int NCH>
+__device__ __forceinline__ void distances(const SearchLaunch& P, Common& c, uint32_t items, uint32_t w,
+                                          int lane) {
+    const IndexView& ix = P.ix;
+    if ((items >> lane) & 1u) {
+        prefetch_l2_bulk(ix.rows + static_cast<uint64_t>(w) * ix.dstride, ix.dstride * 4u);
+        c.degbuf[lane] = __ldg(ix.deg + w);
+    }
+    if (EXACT)
+        dist_exact<NCH>(P, c, items, w, lane);
+    else
+        dist_fast<NCH>(P, c, items, w, lane);
     __syncwarp();
 }
 
@@ -736,25 +780,27 @@ __device__ float query_norm(const float* q, uint32_t D, int lane) {
     return __fsqrt_rn(__fadd_rn(__fadd_rn(a0, a1), __fadd_rn(a2, a3)));
 }
 
-// table sum of one edge's codes (projection.cpp:145-149), serial in l
-__device__ __forceinline__ float code_sum(const float* T, uint32_t L, uint32_t m,
-                                          const uint32_t* cw_global, uint32_t cwp,
-                                          const uint32_t (&cw)[4]) {
+// table sum of one edge's codes (projection.cpp:145-149), serial in l.
+// T is stored with a row stride of 16 (m <= 16), so l*16 + code needs no
+// multiply; fully unrolled for the default subspace counts.
+template <int LL>
+__device__ __forceinline__ float code_sum_fixed(const float* T, const uint32_t (&cw)[4]) {
     float sum = 0.0f;
-    if (cwp <= 4) {
 #pragma unroll
-        for (int wi = 0; wi < 4; ++wi) {
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                const uint32_t l = wi * 8 + t;
-                if (l < L) sum = __fadd_rn(sum, T[l * m + ((cw[wi] >> (4 * t)) & 15u)]);
-            }
-        }
-    } else {
-        for (uint32_t l = 0; l < L; ++l) {
-            const uint32_t word = __ldg(cw_global + (l >> 3));
-            sum = __fadd_rn(sum, T[l * m + ((word >> (4 * (l & 7))) & 15u)]);
-        }
+    for (int l = 0; l < LL; ++l) sum = __fadd_rn(sum, T[l * 16 + ((cw[l >> 3] >> (4 * (l & 7))) & 15u)]);
+    return sum;
+}
+
+__device__ __forceinline__ float code_sum(const float* T, uint32_t L, const uint32_t* cw_global,
+                                          uint32_t cwp, const uint32_t (&cw)[4]) {
+    if (L == 32) return code_sum_fixed<32>(T, cw);
+    if (L == 16) return code_sum_fixed<16>(T, cw);
+    if (L == 8) return code_sum_fixed<8>(T, cw);
+    (void)cwp;
+    float sum = 0.0f;
+    for (uint32_t l = 0; l < L; ++l) {
+        const uint32_t word = __ldg(cw_global + (l >> 3));
+        sum = __fadd_rn(sum, T[l * 16 + ((word >> (4 * (l & 7))) & 15u)]);
     }
     return sum;
 }
@@ -772,7 +818,7 @@ __device__ __forceinline__ void prefetch_block(const IndexView& ix, uint32_t u, 
 }
 
 // routing.cpp:139-204 for W slot `slot`
-template <class TFB, bool EXACT>
+template <class TFB, bool EXACT, int NCH>
 __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, int lane) {
     const IndexView& ix = P.ix;
     const float TAU_HI = 1.0f + 1e-6f;
@@ -834,16 +880,17 @@ __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
 
         // (i) speculative PRT at the group-start radius
         const float adist0 = s.admission_dist();
-        float quot = 0.0f;
+        float quot = 0.0f, tau0 = 0.0f;
         bool spec = false;
         if (cand) {
             if (exact_mode) {
                 spec = true;
             } else {
                 const float tau = prt_threshold(en, duq, adist0);
+                tau0 = tau;
                 if (tau < TAU_HI) {
                     const uint32_t* cp = cw_a + static_cast<uint64_t>(j) * ix.cwp;
-                    const float sum = code_sum(c.T, ix.L, ix.m, cp, ix.cwp, cw);
+                    const float sum = code_sum(c.T, ix.L, cp, ix.cwp, cw);
                     quot = __fdiv_rn(__fdiv_rn(__fsub_rn(sum, bo), duq), cbeta);
                     spec = (tau <= -1.0f) || (quot >= tau);
                 }
@@ -851,7 +898,7 @@ __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
         }
         // (ii) compaction, (iii) exact distances of survivors
         const uint32_t surv = __ballot_sync(FULL, spec);
-        if (surv) distances<EXACT>(P, c, surv, w, lane);
+        if (surv) distances<EXACT, NCH>(P, c, surv, w, lane);
 
         // (iv) in-order replay with the live radius
         uint32_t passed = 0;
@@ -863,10 +910,13 @@ __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
             if (same_j & ((1u << jl) - 1u) & passed) continue;  // marked earlier in this group
             const float en_j = __shfl_sync(FULL, en, jl);
             const float quot_j = __shfl_sync(FULL, quot, jl);
+            const float tau0_j = __shfl_sync(FULL, tau0, jl);
             const uint32_t w_j = __shfl_sync(FULL, w, jl);
             bool pass = true;
             if (!exact_mode) {
-                const float tau = prt_threshold(en_j, duq, s.admission_dist());
+                // the radius is unchanged since the speculative test: reuse its tau
+                const float adist = s.admission_dist();
+                const float tau = adist == adist0 ? tau0_j : prt_threshold(en_j, duq, adist);
                 if (tau >= TAU_HI)
                     pass = false;
                 else if (tau <= -1.0f)
@@ -892,7 +942,7 @@ __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
     }
 }
 
-template <class TFB, bool EXACT>
+template <class TFB, bool EXACT, int NCH>
 __global__ void __launch_bounds__(128, 4) pag_search_kernel(const __grid_constant__ SearchLaunch P) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31;
@@ -1002,14 +1052,14 @@ __global__ void __launch_bounds__(128, 4) pag_search_kernel(const __grid_constan
                 const float* rT = ix.refsT + static_cast<uint64_t>(l) * sub * m + jj;
                 float dot = 0.0f;
                 for (uint32_t cc = 0; cc < sub; ++cc) dot = __fadd_rn(dot, __fmul_rn(xl[cc], __ldg(rT + cc * m)));
-                c.T[e] = dot;
+                c.T[l * 16 + jj] = dot;  // row stride 16 (m <= 16)
             }
         }
         __syncwarp();
 
         for (int g = 0; g < 2; ++g) {
             if (!seed_sel[g]) continue;
-            distances<EXACT>(P, c, seed_sel[g], seed_id[g], lane);
+            distances<EXACT, NCH>(P, c, seed_sel[g], seed_id[g], lane);
             uint32_t rem = seed_sel[g];
             while (rem) {
                 const int t = __ffs(rem) - 1;
@@ -1032,7 +1082,7 @@ __global__ void __launch_bounds__(128, 4) pag_search_kernel(const __grid_constan
                 sel |= 1u << t;
                 --room;
             }
-            distances<EXACT>(P, c, sel, myid, lane);
+            distances<EXACT, NCH>(P, c, sel, myid, lane);
             uint32_t rem = sel;
             while (rem) {
                 const int t = __ffs(rem) - 1;
@@ -1048,7 +1098,7 @@ __global__ void __launch_bounds__(128, 4) pag_search_kernel(const __grid_constan
             while (!c.overflow) {
                 const uint32_t i = s.next_unvisited(lane);
                 if (i == EMPTY) break;
-                expand<TFB, EXACT>(P, c, s, i, lane);
+                expand<TFB, EXACT, NCH>(P, c, s, i, lane);
             }
             if (r + 1 == P.r_max || !s.end_round(c, lane)) break;
         }
@@ -1077,22 +1127,36 @@ __global__ void __launch_bounds__(128, 4) pag_search_kernel(const __grid_constan
     if (lane == 0) P.slot_epoch[slot] = epoch;
 }
 
-template <class TFB, bool EXACT>
-cudaError_t launch_t(const SearchLaunch& L, int grid, size_t smem, cudaStream_t stream) {
-    cudaError_t e = cudaFuncSetAttribute(pag_search_kernel<TFB, EXACT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+template <class TFB, bool EXACT, int NCH>
+cudaError_t launch_t(const SearchLaunch& L, int grid, size_t smem, cudaStream_t stream, int* bps) {
+    auto k = pag_search_kernel<TFB, EXACT, NCH>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    pag_search_kernel<TFB, EXACT><<<grid, L.warps_per_block * 32, smem, stream>>>(L);
+    if (bps) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k, L.warps_per_block * 32, smem);
+    k<<<grid, L.warps_per_block * 32, smem, stream>>>(L);
     return cudaGetLastError();
 }
 
 template <class TFB, bool EXACT>
-cudaError_t occupancy_t(int warps_per_block, size_t smem, int* bps) {
-    cudaError_t e = cudaFuncSetAttribute(pag_search_kernel<TFB, EXACT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, pag_search_kernel<TFB, EXACT>,
-                                                         warps_per_block * 32, smem);
+cudaError_t dispatch_nch(const SearchLaunch& L, int grid, size_t smem, cudaStream_t stream, int* bps) {
+    const uint32_t ds = L.ix.dstride;
+    const bool full = L.ix.padded == ds && ds % 128 == 0;
+    switch (full ? ds / 128 : 0) {
+        case 1: return launch_t<TFB, EXACT, 1>(L, grid, smem, stream, bps);
+        case 4: return launch_t<TFB, EXACT, 4>(L, grid, smem, stream, bps);
+        case 6: return launch_t<TFB, EXACT, 6>(L, grid, smem, stream, bps);
+        case 8: return launch_t<TFB, EXACT, 8>(L, grid, smem, stream, bps);
+        default: return launch_t<TFB, EXACT, 0>(L, grid, smem, stream, bps);
+    }
+}
+
+cudaError_t dispatch(const SearchLaunch& L, int grid, cudaStream_t stream, int* bps) {
+    const size_t smem = static_cast<size_t>(L.warp_smem_bytes) * L.warps_per_block;
+    if (L.b <= 32)
+        return L.exact_dist ? dispatch_nch<TfbReg, true>(L, grid, smem, stream, bps)
+                            : dispatch_nch<TfbReg, false>(L, grid, smem, stream, bps);
+    return L.exact_dist ? dispatch_nch<TfbMem, true>(L, grid, smem, stream, bps)
+                        : dispatch_nch<TfbMem, false>(L, grid, smem, stream, bps);
 }
 
 }  // namespace
@@ -1103,23 +1167,10 @@ size_t search_kernel_smem(const SearchLaunch& L) {
 
 bool search_uses_registers(const SearchLaunch& L) { return L.b <= 32; }
 
-cudaError_t search_occupancy(const SearchLaunch& L, int* blocks_per_sm) {
-    const size_t smem = search_kernel_smem(L);
-    const int wpb = static_cast<int>(L.warps_per_block);
-    if (search_uses_registers(L))
-        return L.exact_dist ? occupancy_t<TfbReg, true>(wpb, smem, blocks_per_sm)
-                            : occupancy_t<TfbReg, false>(wpb, smem, blocks_per_sm);
-    return L.exact_dist ? occupancy_t<TfbMem, true>(wpb, smem, blocks_per_sm)
-                        : occupancy_t<TfbMem, false>(wpb, smem, blocks_per_sm);
-}
+cudaError_t search_occupancy(const SearchLaunch& L, int* blocks_per_sm) { return dispatch(L, 0, nullptr, blocks_per_sm); }
 
 cudaError_t launch_search(const SearchLaunch& L, int grid, cudaStream_t stream) {
-    const size_t smem = search_kernel_smem(L);
-    if (search_uses_registers(L))
-        return L.exact_dist ? launch_t<TfbReg, true>(L, grid, smem, stream)
-                            : launch_t<TfbReg, false>(L, grid, smem, stream);
-    return L.exact_dist ? launch_t<TfbMem, true>(L, grid, smem, stream)
-                        : launch_t<TfbMem, false>(L, grid, smem, stream);
+    return dispatch(L, grid, stream, nullptr);
 }
 
 }  // namespace pagdev
