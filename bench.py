@@ -34,7 +34,6 @@ import os
 import shutil
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -43,6 +42,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 from paper_2603_06660_b200.fvecs import CONFIGS, gaussian_mixture, read_fvecs, write_fvecs  # noqa: E402
+from paper_2603_06660_b200.shard import broadcast_int, max_over_ranks  # noqa: E402
 
 REF_BIN = os.path.join(ROOT, "oracle", "_ref", "pag_ref")
 SEEDS = dict(centre=7, base=1, query=2)
@@ -281,10 +281,7 @@ def run_pag(args, cfg, paths, rank, world, local_rank, threads, dist):
                 json.dump({"efS": efs, "sweep": sweep}, f)
         r = ix.search_batch(queries, pag.SearchParams(K=K, efS=efs, exact_dist=not args.fast_dist))
         recall = pag.mean_recall(r.ids, r.n_out, gt_ids, gt_sq, K)
-    if dist is not None:
-        t = torch.tensor([efs], dtype=torch.int64, device=dev)
-        dist.broadcast(t, 0)
-        efs = int(t.item())
+    efs = broadcast_int(efs, dist, dev)  # control plane only
     params = pag.SearchParams(K=K, efS=efs, exact_dist=not args.fast_dist)
 
     # device-resident batch
@@ -316,9 +313,7 @@ def run_pag(args, cfg, paths, rank, world, local_rank, threads, dist):
     total_ms = ev[0].elapsed_time(ev[-1])
     if dist is not None:
         dist.barrier()
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = max_over_ranks(total_ms, dist, dev)
     ms_per_step = total_ms / args.steps
     value = world * nq * args.steps / (total_ms / 1e3)
 
@@ -343,10 +338,7 @@ def run_pag(args, cfg, paths, rank, world, local_rank, threads, dist):
     for _ in range(e2e_steps):
         ix.search_batch(qh, params)
     e2e_s = max(time.perf_counter() - t, 1e-9)
-    if dist is not None:
-        tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_s = float(tt.item())
+    e2e_s = max_over_ranks(e2e_s, dist, dev)
     e2e_qps = world * nq * e2e_steps / e2e_s
     h2d = nq * queries.shape[1] * 4
     d2h = nq * K * 8 + nq * 4 + nq * 8 * 4

@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpag_gpu.so")
+LIB_PATH = os.environ.get("PAG_GPU_LIB") or os.path.join(HERE, "libpag_gpu.so")
 
 PAG_GPU_OK = 0
 PAG_GPU_EINVAL = 1

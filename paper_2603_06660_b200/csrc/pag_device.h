@@ -79,6 +79,7 @@ struct SearchLaunch {
     uint32_t off_rl, rl_in_smem;
     uint32_t off_merge, merge_in_smem;
     uint32_t warps_per_block;
+    uint32_t tune;  // experiment bits (PAG_GPU_TUNE): 1 admit-time adjacency prefetch, 2 next-node prefetch
 };
 
 size_t search_kernel_smem(const SearchLaunch& L);

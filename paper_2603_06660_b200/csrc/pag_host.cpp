@@ -476,7 +476,10 @@ struct Plan {
 };
 
 constexpr int kWarpsPerBlock = 4;
-constexpr uint32_t kWarpSmemBudget = 14 * 1024;
+#ifndef PAG_WARP_SMEM_BUDGET
+#define PAG_WARP_SMEM_BUDGET (14 * 1024)
+#endif
+constexpr uint32_t kWarpSmemBudget = PAG_WARP_SMEM_BUDGET;
 
 uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 
@@ -494,8 +497,10 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     L.nq = nq;
     L.ix = ix.view(r);
     L.warps_per_block = kWarpsPerBlock;
+    L.tune = std::getenv("PAG_GPU_TUNE") ? static_cast<uint32_t>(std::atoi(std::getenv("PAG_GPU_TUNE"))) : 0u;
     L.stage_rows = 4;
     L.hash_log2 = p.efS <= 200 ? 10 : 11;
+    if (const char* e = std::getenv("PAG_GPU_HASH_LOG2")) L.hash_log2 = static_cast<uint32_t>(std::atoi(e));
     const uint32_t b = L.b, capr = std::max(1u, p.efS);
     const bool regs = pagdev::search_uses_registers(L);
     // fixed smem regions

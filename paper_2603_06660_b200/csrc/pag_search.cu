@@ -829,7 +829,7 @@ __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
     // speculative L2 prefetch of the node expanded next if nothing nearer is
     // admitted meanwhile (adjacency is the head of the next dependency chain)
     {
-        const uint32_t nx = s.next_unvisited(lane);
+        const uint32_t nx = (P.tune & 2u) ? s.next_unvisited(lane) : EMPTY;
         if (nx != EMPTY) {
             const uint32_t nid = s.entry_id(nx), ndeg = s.entry_deg(nx);
             if (lane == 0) prefetch_block(ix, nid, ndeg);
@@ -931,10 +931,14 @@ __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
             const float sq_j = c.sqbuf[jl];
             const uint32_t deg_j = c.degbuf[jl];
             mark(c, w_j, lane);
-            if (sq_j < s.admission_sq())
+            if (sq_j < s.admission_sq()) {
                 s.admit(w_j, sq_j, deg_j, lane);
-            else
+                // an admitted node is usually expanded later: start its
+                // adjacency on the way to L2 now (hides the next dependency)
+                if ((P.tune & 1u) && lane == 0) prefetch_block(ix, w_j, deg_j);
+            } else {
                 s.push_fp(w_j, sq_j, deg_j, lane);
+            }
         }
         const bool not_test = cand && ((same & lt & passed) != 0u);
         c.n_test += __popc(cand_mask) - __popc(__ballot_sync(FULL, not_test));
@@ -943,7 +947,10 @@ __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
 }
 
 template <class TFB, bool EXACT, int NCH>
-__global__ void __launch_bounds__(128, 4) pag_search_kernel(const __grid_constant__ SearchLaunch P) {
+#ifndef PAG_MIN_BLOCKS
+#define PAG_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const __grid_constant__ SearchLaunch P) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
