@@ -526,7 +526,9 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     if (total() > kWarpSmemBudget) rl_s = false;
     if (total() > kWarpSmemBudget) m_s = false;
     if (total() > kWarpSmemBudget) r_s = false;
-    if (total() > kWarpSmemBudget) w_s = false;
+    // the working set is scanned on every expansion: keep it on-chip even at
+    // the cost of occupancy (large b), up to 48 KB per warp
+    if (total() > std::max<uint64_t>(kWarpSmemBudget, std::min<uint64_t>(48 * 1024, off + szW))) w_s = false;
     uint64_t goff = 0;
     auto place = [&](bool in_smem, uint64_t sz, uint32_t* o, uint32_t* flag) {
         *flag = in_smem;
