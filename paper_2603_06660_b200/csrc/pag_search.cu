@@ -817,47 +817,9 @@ __device__ __forceinline__ void prefetch_block(const IndexView& ix, uint32_t u, 
     prefetch_l2_bulk(blk + 16u * S, 4u * ix.cwp * deg);
 }
 
-// First 32-edge group of the node predicted to be expanded next, loaded into
-// registers one expansion ahead (prediction: the nearest unvisited W entry
-// other than the one being expanded; wrong when an admission beats it).
-struct Lookahead {
-    uint32_t u;  // EMPTY = none
-    uint32_t w;
-    float en, cb, bo;
-    uint32_t cw[4];
-};
-
-__device__ __forceinline__ void load_group(const IndexView& ix, uint32_t u, uint32_t deg, uint32_t g0, int lane,
-                                           uint32_t& w, float& en, float& cb, float& bo, uint32_t (&cw)[4]) {
-    const uint8_t* blk = ix.adj + static_cast<uint64_t>(u) * ix.block_bytes;
-    const uint32_t S = ix.slot_stride;
-    const uint32_t j = g0 + lane;
-    w = 0;
-    en = 0.f;
-    cb = 1.f;
-    bo = 0.f;
-    cw[0] = cw[1] = cw[2] = cw[3] = 0;
-    if (j < deg) {
-        w = __ldg(reinterpret_cast<const uint32_t*>(blk) + j);
-        en = __ldg(reinterpret_cast<const float*>(blk + 4u * S) + j);
-        cb = __ldg(reinterpret_cast<const float*>(blk + 8u * S) + j);
-        bo = __ldg(reinterpret_cast<const float*>(blk + 12u * S) + j);
-        const uint32_t* cp = reinterpret_cast<const uint32_t*>(blk + 16u * S) + static_cast<uint64_t>(j) * ix.cwp;
-        if (ix.cwp == 4) {
-            const uint4 v = __ldg(reinterpret_cast<const uint4*>(cp));
-            cw[0] = v.x; cw[1] = v.y; cw[2] = v.z; cw[3] = v.w;
-        } else if (ix.cwp == 2) {
-            const uint2 v = __ldg(reinterpret_cast<const uint2*>(cp));
-            cw[0] = v.x; cw[1] = v.y;
-        } else if (ix.cwp == 1) {
-            cw[0] = __ldg(cp);
-        }
-    }
-}
-
 // routing.cpp:139-204 for W slot `slot`
 template <class TFB, bool EXACT, int NCH>
-__device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, int lane, Lookahead& la) {
+__device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, int lane) {
     const IndexView& ix = P.ix;
     const float TAU_HI = 1.0f + 1e-6f;
     uint32_t u, deg;
@@ -871,20 +833,6 @@ __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
         if (nx != EMPTY) {
             const uint32_t nid = s.entry_id(nx), ndeg = s.entry_deg(nx);
             if (lane == 0) prefetch_block(ix, nid, ndeg);
-        }
-    }
-    // consume the register lookahead if it predicted this node, then start
-    // the next prediction's loads (in flight during this whole expansion)
-    const bool la_hit = la.u == u;
-    const uint32_t la_w = la.w;
-    const float la_en = la.en, la_cb = la.cb, la_bo = la.bo;
-    const uint32_t la_cw0 = la.cw[0], la_cw1 = la.cw[1], la_cw2 = la.cw[2], la_cw3 = la.cw[3];
-    la.u = EMPTY;
-    if (P.tune & 4u) {
-        const uint32_t nx = s.next_unvisited(lane);
-        if (nx != EMPTY) {
-            la.u = s.entry_id(nx);
-            load_group(ix, la.u, s.entry_deg(nx), 0, lane, la.w, la.en, la.cb, la.bo, la.cw);
         }
     }
     ++c.n_visited;
@@ -906,13 +854,7 @@ __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
         uint32_t w = 0;
         float en = 0.f, cbeta = 1.f, bo = 0.f;
         uint32_t cw[4] = {0, 0, 0, 0};
-        if (g0 == 0 && la_hit) {
-            w = la_w;
-            en = la_en;
-            cbeta = la_cb;
-            bo = la_bo;
-            cw[0] = la_cw0; cw[1] = la_cw1; cw[2] = la_cw2; cw[3] = la_cw3;
-        } else if (active) {
+        if (active) {
             w = __ldg(tg + j);
             en = __ldg(en_a + j);
             cbeta = __ldg(cb_a + j);
@@ -1159,13 +1101,11 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
         }
 
         // ---- rounds (routing.cpp:229-240)
-        Lookahead la;
-        la.u = EMPTY;
         for (uint32_t r = 0; r < P.r_max && !c.overflow; ++r) {
             while (!c.overflow) {
                 const uint32_t i = s.next_unvisited(lane);
                 if (i == EMPTY) break;
-                expand<TFB, EXACT, NCH>(P, c, s, i, lane, la);
+                expand<TFB, EXACT, NCH>(P, c, s, i, lane);
             }
             if (r + 1 == P.r_max || !s.end_round(c, lane)) break;
         }
