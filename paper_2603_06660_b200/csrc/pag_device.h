@@ -103,6 +103,34 @@ struct GtLaunch {
     uint32_t* scratch_id;
 };
 cudaError_t launch_ground_truth(const GtLaunch& g, cudaStream_t stream);
+
+// Tensor-core ground truth (pag_gt_tc.cu): TF32 tcgen05 candidate GEMM with a
+// fused per-split top-C epilogue, exact reference-order re-rank, certificate.
+struct GtTcLaunch {
+    const void* tmA;  // CUtensorMap over queries (nq x padded, row pitch dstride*4)
+    const void* tmB;  // CUtensorMap over base rows (n x padded)
+    const float* base;
+    uint64_t n;
+    uint32_t padded, dstride;
+    const float* queries;  // nq x dstride, zero padded
+    uint32_t nq, k, nsplit, C;
+    uint64_t rows_per_split;  // multiple of gt_tc_block_n()
+    float* qnorm;             // nq scratch (squared norms)
+    const float* bnorm;       // n squared norms of the base rows
+    float max_bnorm;          // max squared base norm
+    float* cand_d;            // nq x nsplit x C
+    uint32_t* cand_id;        // nq x nsplit x C
+    float* cand_thr;          // nq x nsplit
+    uint32_t* out_ids;        // nq x k
+    float* out_sq;            // nq x k
+    uint32_t* uncertified;    // nq flags: 1 = re-run exactly
+};
+cudaError_t launch_gt_tc(const GtTcLaunch& g, cudaStream_t stream);
+size_t gt_tc_smem_bytes();
+uint32_t gt_tc_cmax();
+uint32_t gt_tc_block_n();
+uint32_t gt_tc_block_k();
+uint32_t gt_tc_block_m();
 size_t gt_scratch_elems(uint64_t n, uint32_t nq, uint32_t k);
 
 }  // namespace pagdev

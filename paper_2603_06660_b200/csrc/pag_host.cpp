@@ -7,6 +7,7 @@
 //   build_reference_set   proj/src/projection.cpp:13-74
 //   search                proj/src/routing.cpp:206-261
 //   ground_truth          proj/src/bench.cpp:18-53
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <fcntl.h>
 #include <sys/mman.h>
@@ -166,6 +167,7 @@ struct Replica {
     uint8_t* adj = nullptr;
     float* refsT = nullptr;
     uint32_t* entries = nullptr;
+    float* bnorm = nullptr;  // squared row norms (from the file's cached norms), GT only
     size_t bytes = 0;
     // search scratch
     uint64_t* gtab = nullptr;
@@ -213,6 +215,8 @@ struct pag_gpu_index {
     std::vector<uint32_t> entries;
     uint32_t maxdeg = 0, cb = 0, cwp = 0, slot_stride = 0, block_bytes = 0, sub_dim = 0;
     uint64_t total_edges = 0;
+    float max_bnorm = 0.0f;        // max squared row norm
+    uint64_t gt_uncertified = 0;   // tensor-core GT queries re-run exactly (diagnostic)
     std::vector<float> refs;
     std::vector<Replica> reps;
     std::mutex mu;
@@ -248,7 +252,7 @@ void free_replica(Replica& r) {
                     static_cast<void*>(r.refsT), static_cast<void*>(r.entries),
                     static_cast<void*>(r.gtab), static_cast<void*>(r.slot_epoch),
                     static_cast<void*>(r.gscratch), static_cast<void*>(r.qcounter),
-                    static_cast<void*>(r.d_q), static_cast<void*>(r.d_out)})
+                    static_cast<void*>(r.d_q), static_cast<void*>(r.d_out), static_cast<void*>(r.bnorm)})
         dev_free(p);
     if (r.h_pin) cudaFreeHost(r.h_pin);
     if (r.stream) cudaStreamDestroy(r.stream);
@@ -462,6 +466,23 @@ std::unique_ptr<pag_gpu_index> open_index(const char* path, uint32_t device_mask
             buf ^= 1;
         }
         for (auto& r : ix->reps) cuda_check(cudaStreamSynchronize(r.stream), "rows upload");
+        // squared norms for the tensor-core ground truth (cached norms are the
+        // stored rows' vec_norm, builder.cpp:489-491)
+        if (!ix->reps.empty()) {
+            std::vector<float> bn(n);
+            const uint8_t* norms = rows + 4ull * ix->padded * n;
+            for (uint64_t i = 0; i < n; ++i) {
+                float v;
+                std::memcpy(&v, norms + 4 * i, 4);
+                bn[i] = v * v;
+                ix->max_bnorm = std::max(ix->max_bnorm, bn[i]);
+            }
+            for (auto& r : ix->reps) {
+                cudaSetDevice(r.device);
+                dev_alloc(&r.bnorm, 4ull * std::max<uint64_t>(1, n));
+                cuda_check(cudaMemcpy(r.bnorm, bn.data(), 4ull * n, cudaMemcpyHostToDevice), "H2D norms");
+            }
+        }
     }
     return ix;
 }
@@ -671,51 +692,138 @@ void search_on_replica(pag_gpu_index& ix, Replica& r, const pag_search_params& p
 // ---------------------------------------------------------------------------
 // Ground truth driver
 // ---------------------------------------------------------------------------
-void ground_truth_on_replica(pag_gpu_index& ix, Replica& r, const float* q, uint64_t nq, uint32_t k,
-                             uint32_t* ids, float* sq) {
-    cuda_check(cudaSetDevice(r.device), "cudaSetDevice");
-    if (nq == 0 || k == 0) return;
-    const uint32_t kk = static_cast<uint32_t>(std::min<uint64_t>(k, ix.n));
-    std::vector<float> qp(nq * ix.dstride, 0.0f);
-    for (uint64_t i = 0; i < nq; ++i) std::memcpy(&qp[i * ix.dstride], q + i * ix.dim, 4ull * ix.dim);
-    float* d_q = nullptr;
-    uint32_t* d_ids = nullptr;
-    float* d_sq = nullptr;
-    float* s_sq = nullptr;
-    const size_t se = pagdev::gt_scratch_elems(ix.n, static_cast<uint32_t>(nq), kk);
-    struct F {
-        void* p[5];
-        ~F() {
-            for (void* x : p) dev_free(x);
-        }
-    } fr{{nullptr, nullptr, nullptr, nullptr, nullptr}};
-    dev_alloc(&d_q, 4 * qp.size());
-    fr.p[0] = d_q;
-    dev_alloc(&d_ids, 4ull * nq * kk);
-    fr.p[1] = d_ids;
-    dev_alloc(&d_sq, 4ull * nq * kk);
-    fr.p[2] = d_sq;
-    dev_alloc(&s_sq, 4 * se);
-    fr.p[3] = s_sq;
-    cuda_check(cudaMemcpyAsync(d_q, qp.data(), 4 * qp.size(), cudaMemcpyHostToDevice, r.stream), "H2D");
+struct DevBuf {  // scoped device allocation
+    void* p = nullptr;
+    explicit DevBuf(size_t bytes) { cuda_check(cudaMalloc(&p, bytes ? bytes : 16), "cudaMalloc"); }
+    ~DevBuf() { dev_free(p); }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+// exact SIMT ground truth (pag_gt.cu) for nq padded queries on the device
+void exact_gt(const pag_gpu_index& ix, Replica& r, const float* d_q, uint32_t nq, uint32_t kk, uint32_t* d_ids,
+              float* d_sq) {
+    DevBuf scratch(4 * pagdev::gt_scratch_elems(ix.n, nq, kk));
     pagdev::GtLaunch g{};
     g.base = r.rows;
     g.n = ix.n;
     g.padded = ix.padded;
     g.dstride = ix.dstride;
     g.queries = d_q;
-    g.nq = static_cast<uint32_t>(nq);
+    g.nq = nq;
     g.k = kk;
     g.out_ids = d_ids;
     g.out_sq = d_sq;
-    g.scratch_sq = s_sq;
+    g.scratch_sq = scratch.as<float>();
     g.scratch_id = nullptr;
     cuda_check(pagdev::launch_ground_truth(g, r.stream), "ground truth kernels");
+    cuda_check(cudaStreamSynchronize(r.stream), "ground truth");
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+CUtensorMap tensor_map_rows(const float* base, uint64_t rows, uint32_t padded, uint32_t dstride, uint32_t box_rows) {
+    static EncodeTiledFn encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        cuda_check(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr),
+                   "cuTensorMapEncodeTiled lookup");
+        if (!fn || qr != cudaDriverEntryPointSuccess) throw_err(PAG_GPU_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<EncodeTiledFn>(fn);
+    }
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {padded, rows};
+    const cuuint64_t strides[1] = {4ull * dstride};
+    const cuuint32_t box[2] = {pagdev::gt_tc_block_k(), box_rows};
+    const cuuint32_t es[2] = {1, 1};
+    if (encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        throw_err(PAG_GPU_ECUDA, "cuTensorMapEncodeTiled failed");
+    return m;
+}
+
+// bench.cpp:18-53. k <= 32: tensor-core candidates + exact re-rank +
+// certificate (uncertified queries re-run exactly); otherwise exact SIMT.
+void ground_truth_on_replica(pag_gpu_index& ix, Replica& r, const float* q, uint64_t nq, uint32_t k,
+                             uint32_t* ids, float* sq) {
+    cuda_check(cudaSetDevice(r.device), "cudaSetDevice");
+    if (nq == 0 || k == 0) return;
+    const uint32_t kk = static_cast<uint32_t>(std::min<uint64_t>(k, ix.n));
+    const uint32_t nqu = static_cast<uint32_t>(nq);
+    std::vector<float> qp(nq * ix.dstride, 0.0f);
+    for (uint64_t i = 0; i < nq; ++i) std::memcpy(&qp[i * ix.dstride], q + i * ix.dim, 4ull * ix.dim);
+    DevBuf d_q(4 * qp.size()), d_ids(4ull * nq * kk), d_sq(4ull * nq * kk);
+    cuda_check(cudaMemcpy(d_q.p, qp.data(), 4 * qp.size(), cudaMemcpyHostToDevice), "H2D");
+    const bool tc = kk <= pagdev::gt_tc_cmax() / 2 && r.bnorm && !std::getenv("PAG_GPU_GT_EXACT");
+    std::vector<uint32_t> redo;
+    if (tc) {
+        const uint32_t C = pagdev::gt_tc_cmax(), BN = pagdev::gt_tc_block_n();
+        const uint32_t mt = (nqu + pagdev::gt_tc_block_m() - 1) / pagdev::gt_tc_block_m();
+        const uint64_t ntile = (ix.n + BN - 1) / BN;
+        uint32_t ns = std::max<uint32_t>(1, std::min<uint32_t>(64, (4u * r.num_sms + mt / 2) / mt));
+        const uint64_t rps = ((ntile + ns - 1) / ns) * BN;
+        ns = static_cast<uint32_t>((ix.n + rps - 1) / rps);
+        CUtensorMap tmA = tensor_map_rows(d_q.as<float>(), nq, ix.padded, ix.dstride, pagdev::gt_tc_block_m());
+        CUtensorMap tmB = tensor_map_rows(r.rows, ix.n, ix.padded, ix.dstride, BN);
+        DevBuf qn(4ull * nq), cd(4ull * nq * ns * C), cid(4ull * nq * ns * C), cthr(4ull * nq * ns), unc(4ull * nq);
+        pagdev::GtTcLaunch g{};
+        g.tmA = &tmA;
+        g.tmB = &tmB;
+        g.base = r.rows;
+        g.n = ix.n;
+        g.padded = ix.padded;
+        g.dstride = ix.dstride;
+        g.queries = d_q.as<float>();
+        g.nq = nqu;
+        g.k = kk;
+        g.nsplit = ns;
+        g.C = C;
+        g.rows_per_split = rps;
+        g.qnorm = qn.as<float>();
+        g.bnorm = r.bnorm;
+        g.max_bnorm = ix.max_bnorm;
+        g.cand_d = cd.as<float>();
+        g.cand_id = cid.as<uint32_t>();
+        g.cand_thr = cthr.as<float>();
+        g.out_ids = d_ids.as<uint32_t>();
+        g.out_sq = d_sq.as<float>();
+        g.uncertified = unc.as<uint32_t>();
+        cuda_check(pagdev::launch_gt_tc(g, r.stream), "tensor-core ground truth");
+        std::vector<uint32_t> flags(nq);
+        cuda_check(cudaMemcpyAsync(flags.data(), unc.p, 4ull * nq, cudaMemcpyDeviceToHost, r.stream), "D2H");
+        cuda_check(cudaStreamSynchronize(r.stream), "tensor-core ground truth");
+        for (uint32_t i = 0; i < nqu; ++i)
+            if (flags[i]) redo.push_back(i);
+        ix.gt_uncertified += redo.size();
+    } else {
+        exact_gt(ix, r, d_q.as<float>(), nqu, kk, d_ids.as<uint32_t>(), d_sq.as<float>());
+    }
     std::vector<uint32_t> hi(nq * kk);
     std::vector<float> hs(nq * kk);
-    cuda_check(cudaMemcpyAsync(hi.data(), d_ids, 4 * hi.size(), cudaMemcpyDeviceToHost, r.stream), "D2H");
-    cuda_check(cudaMemcpyAsync(hs.data(), d_sq, 4 * hs.size(), cudaMemcpyDeviceToHost, r.stream), "D2H");
-    cuda_check(cudaStreamSynchronize(r.stream), "ground truth");
+    cuda_check(cudaMemcpy(hi.data(), d_ids.p, 4 * hi.size(), cudaMemcpyDeviceToHost), "D2H");
+    cuda_check(cudaMemcpy(hs.data(), d_sq.p, 4 * hs.size(), cudaMemcpyDeviceToHost), "D2H");
+    if (!redo.empty()) {  // exact fallback for the uncertified queries
+        const uint32_t nr = static_cast<uint32_t>(redo.size());
+        std::vector<float> qr(static_cast<size_t>(nr) * ix.dstride);
+        for (uint32_t i = 0; i < nr; ++i)
+            std::memcpy(&qr[static_cast<size_t>(i) * ix.dstride], &qp[static_cast<size_t>(redo[i]) * ix.dstride],
+                        4ull * ix.dstride);
+        DevBuf rq(4 * qr.size()), rids(4ull * nr * kk), rsq(4ull * nr * kk);
+        cuda_check(cudaMemcpy(rq.p, qr.data(), 4 * qr.size(), cudaMemcpyHostToDevice), "H2D");
+        exact_gt(ix, r, rq.as<float>(), nr, kk, rids.as<uint32_t>(), rsq.as<float>());
+        std::vector<uint32_t> ri(static_cast<size_t>(nr) * kk);
+        std::vector<float> rs(static_cast<size_t>(nr) * kk);
+        cuda_check(cudaMemcpy(ri.data(), rids.p, 4 * ri.size(), cudaMemcpyDeviceToHost), "D2H");
+        cuda_check(cudaMemcpy(rs.data(), rsq.p, 4 * rs.size(), cudaMemcpyDeviceToHost), "D2H");
+        for (uint32_t i = 0; i < nr; ++i) {
+            std::memcpy(&hi[static_cast<size_t>(redo[i]) * kk], &ri[static_cast<size_t>(i) * kk], 4ull * kk);
+            std::memcpy(&hs[static_cast<size_t>(redo[i]) * kk], &rs[static_cast<size_t>(i) * kk], 4ull * kk);
+        }
+    }
     for (uint64_t i = 0; i < nq; ++i) {
         std::memcpy(ids + i * k, &hi[i * kk], 4ull * kk);
         std::memcpy(sq + i * k, &hs[i * kk], 4ull * kk);
@@ -794,10 +902,10 @@ int pag_gpu_close(pag_gpu_index* ix) {
 int pag_gpu_info(const pag_gpu_index* ix, uint64_t* info, size_t n_info) {
     return guarded([&] {
         if (!ix || !info) throw_err(PAG_GPU_EINVAL, "null argument");
-        const uint64_t v[12] = {ix->n, ix->dim, ix->padded, ix->L, ix->m, ix->M, ix->metric,
+        const uint64_t v[13] = {ix->n, ix->dim, ix->padded, ix->L, ix->m, ix->M, ix->metric,
                                 ix->entries.size(), ix->seed, ix->total_edges, ix->reps.size(),
-                                ix->reps.empty() ? 0 : ix->reps[0].bytes};
-        for (size_t i = 0; i < n_info && i < 12; ++i) info[i] = v[i];
+                                ix->reps.empty() ? 0 : ix->reps[0].bytes, ix->gt_uncertified};
+        for (size_t i = 0; i < n_info && i < 13; ++i) info[i] = v[i];
     });
 }
 

@@ -139,6 +139,24 @@ def test_ground_truth_bitexact(pag, built, name, k):
     assert np.array_equal(gi, oi) and np.array_equal(gs.view(np.uint32), os_.view(np.uint32))
 
 
+@pytest.mark.parametrize("name,k", [("euc48", 1), ("euc48", 10), ("euc48", 32), ("tail10", 16),
+                                    ("cos20", 8), ("deg64", 25)])
+def test_tensor_core_ground_truth_equals_exact(pag, built, monkeypatch, name, k):
+    """tcgen05 TF32 candidates + exact re-rank + certificate (k <= 32) gives
+    the same ids and bits as the exact SIMT kernel and the oracle."""
+    fx = built(name)
+    ix = gpu_index(pag, fx["index"])
+    ti, ts = ix.ground_truth(fx["queries"], k)
+    monkeypatch.setenv("PAG_GPU_GT_EXACT", "1")
+    ei, es = ix.ground_truth(fx["queries"], k)
+    assert np.array_equal(ti, ei) and np.array_equal(ts.view(np.uint32), es.view(np.uint32))
+    oix = O.OracleIndex(fx["index"])
+    q = np.zeros((fx["queries"].shape[0], oix.padded), np.float32)
+    q[:, :oix.dim] = fx["queries"]
+    oi, _ = O.ground_truth(oix.rows(), q, k)
+    assert np.array_equal(ti, oi)
+
+
 def test_device_path_matches_host_path(pag, built):
     import torch
     fx = built("euc48")
