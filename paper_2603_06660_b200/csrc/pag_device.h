@@ -87,6 +87,8 @@ size_t search_kernel_smem(const SearchLaunch& L);
 bool search_uses_registers(const SearchLaunch& L);
 cudaError_t launch_search(const SearchLaunch& L, int grid, cudaStream_t stream);
 cudaError_t search_occupancy(const SearchLaunch& L, int* blocks_per_sm);
+// PAG_PHASE_TIMING builds only: summed per-warp cycles per phase
+void search_phase_cycles(unsigned long long* out8, bool reset);
 
 // Exact brute-force ground truth (bench.cpp:18-53): reference-order fp32
 // distances, top-k by (sq, id).

@@ -999,6 +999,9 @@ int pag_gpu_ground_truth(pag_gpu_index* ix, const float* queries, uint64_t nq, u
 
 const char* pag_gpu_last_error(void) { return g_err.c_str(); }
 
+// diagnostic (PAG_PHASE_TIMING builds): per-phase summed warp cycles
+void pag_gpu_phase_cycles(unsigned long long* out8, int reset) { pagdev::search_phase_cycles(out8, reset != 0); }
+
 const char* pag_gpu_version(void) { return "pag_gpu 0.1 (sm_100a)"; }
 
 }  // extern "C"

@@ -38,6 +38,14 @@
 namespace pagdev {
 namespace {
 
+#ifdef PAG_PHASE_TIMING
+// per-warp cycle accounting of the expansion phases (diagnostic build only)
+__device__ unsigned long long g_phase[8];
+#define PT(k) do { long long t_ = clock64(); c.pt_acc[k] += t_ - c.pt_t0; c.pt_t0 = t_; } while (0)
+#else
+#define PT(k) do { } while (0)
+#endif
+
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint32_t EMPTY = 0xffffffffu;
 constexpr uint32_t VISITED = 0x80000000u;
@@ -107,6 +115,9 @@ struct Common {
     uint32_t rl_cur, rl_size, cap_r;
     // counters (routing.hpp:24-34 + edges_scanned)
     uint32_t n_exact, n_test, n_pass, n_visited, n_edges;
+#ifdef PAG_PHASE_TIMING
+    long long pt_t0, pt_acc[8];
+#endif
 
     __device__ Arr rl_cur_arr() const { return rl_cur ? rlB : rlA; }
     __device__ Arr rl_next_arr() const { return rl_cur ? rlA : rlB; }
@@ -158,6 +169,29 @@ __device__ __forceinline__ void mark(Common& c, uint32_t id, int lane) {
         ++c.gt_count;
     }
     __syncwarp();
+}
+
+// marks the targets of the lanes in `lanes` (distinct ids). Parallel
+// atomicCAS probing while everything fits the smem half-load budget, else the
+// sequential path (HBM spill, overflow detection).
+__device__ __forceinline__ void mark_many(Common& c, uint32_t lanes, uint32_t w, int lane) {
+    const uint32_t np = __popc(lanes);
+    if (c.hs_count + np <= (1u << c.hs_log2) / 2) {
+        if ((lanes >> lane) & 1u) {
+            const uint32_t mask = (1u << c.hs_log2) - 1;
+            uint32_t h = hslot(w, c.hs_log2);
+            while (atomicCAS(&c.hs[h], EMPTY, w) != EMPTY) h = (h + 1) & mask;
+        }
+        c.hs_count += np;
+        __syncwarp();
+        return;
+    }
+    uint32_t rem = lanes;
+    while (rem) {
+        const int j = __ffs(rem) - 1;
+        rem &= rem - 1;
+        mark(c, __shfl_sync(FULL, w, j), lane);
+    }
 }
 
 // number of entries of sorted a[0..n) strictly less than (v, id)
@@ -721,23 +755,33 @@ __device__ void dist_fast(const SearchLaunch& P, Common& c, uint32_t items, uint
         float2 part[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) part[r] = make_float2(0.f, 0.f);
-#pragma unroll 2
+        // one chunk of look-ahead (rows past nb alias row 0: no load predicates)
+        float4 cur[4], nxt[4];
+        const bool in0 = NCH || 4u * lane < DS;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) cur[r] = in0 ? ldg_f4(rp[r]) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll(NCH ? NCH : 1)
         for (uint32_t ch = 0; ch < nch; ++ch) {
             const uint32_t base = 128u * ch;
+            const bool inn = NCH ? (ch + 1 < nch) : (base + 128u + 4u * lane < DS);
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                nxt[r] = inn ? ldg_f4(rp[r] + base + 128u) : make_float4(0.f, 0.f, 0.f, 0.f);
             if (NCH || base + 4u * lane < DS) {
                 const float4 qv = *reinterpret_cast<const float4*>(c.q + base + 4u * lane);
                 const float2 nqlo = make_float2(-qv.x, -qv.y), nqhi = make_float2(-qv.z, -qv.w);
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
                     if (r < nb) {
-                        const float4 v = ldg_f4(rp[r] + base);
-                        const float2 dlo = __fadd2_rn(make_float2(v.x, v.y), nqlo);
-                        const float2 dhi = __fadd2_rn(make_float2(v.z, v.w), nqhi);
+                        const float2 dlo = __fadd2_rn(make_float2(cur[r].x, cur[r].y), nqlo);
+                        const float2 dhi = __fadd2_rn(make_float2(cur[r].z, cur[r].w), nqhi);
                         part[r] = __ffma2_rn(dlo, dlo, part[r]);
                         part[r] = __ffma2_rn(dhi, dhi, part[r]);
                     }
                 }
             }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) cur[r] = nxt[r];
         }
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
@@ -870,7 +914,9 @@ __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
                 cw[0] = __ldg(cp);
             }
         }
+        PT(2);
         const bool cand = active && !marked(c, w);
+        PT(3);
         const uint32_t cand_mask = __ballot_sync(FULL, cand);
         // duplicate targets inside the group (reference order: a later copy
         // is skipped when an earlier copy passed and marked it)
@@ -898,7 +944,9 @@ __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
         }
         // (ii) compaction, (iii) exact distances of survivors
         const uint32_t surv = __ballot_sync(FULL, spec);
+        PT(4);
         if (surv) distances<EXACT, NCH>(P, c, surv, w, lane);
+        PT(5);
 
         // (iv) in-order replay with the live radius
         uint32_t passed = 0;
@@ -930,7 +978,7 @@ __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
             ++c.n_exact;
             const float sq_j = c.sqbuf[jl];
             const uint32_t deg_j = c.degbuf[jl];
-            mark(c, w_j, lane);
+            if (P.tune & 8u) mark(c, w_j, lane);  // (diagnostic) sequential marking
             if (sq_j < s.admission_sq()) {
                 s.admit(w_j, sq_j, deg_j, lane);
                 // an admitted node is usually expanded later: start its
@@ -940,8 +988,13 @@ __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
                 s.push_fp(w_j, sq_j, deg_j, lane);
             }
         }
+        // marks of this group's passes (routing.cpp:183). Later lookups come
+        // from the next group/expansion only (in-group duplicates are resolved
+        // by `same`), so the inserts are deferred and done in parallel.
+        if (passed && !(P.tune & 8u)) mark_many(c, passed, w, lane);
         const bool not_test = cand && ((same & lt & passed) != 0u);
         c.n_test += __popc(cand_mask) - __popc(__ballot_sync(FULL, not_test));
+        PT(6);
         __syncwarp();
     }
 }
@@ -960,6 +1013,10 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
     const IndexView& ix = P.ix;
 
     Common c;
+#ifdef PAG_PHASE_TIMING
+    c.pt_t0 = clock64();
+    for (int k = 0; k < 8; ++k) c.pt_acc[k] = 0;
+#endif
     c.q = reinterpret_cast<float*>(sw + P.off_q);
     c.T = reinterpret_cast<float*>(sw + P.off_T);
     c.sqbuf = reinterpret_cast<float*>(sw + P.off_sqbuf);
@@ -1058,7 +1115,15 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
                 const float* xl = c.q + l * sub;
                 const float* rT = ix.refsT + static_cast<uint64_t>(l) * sub * m + jj;
                 float dot = 0.0f;
-                for (uint32_t cc = 0; cc < sub; ++cc) dot = __fadd_rn(dot, __fmul_rn(xl[cc], __ldg(rT + cc * m)));
+                uint32_t cc = 0;
+                for (; cc + 8 <= sub; cc += 8) {  // 8 independent loads in flight, serial sum
+                    float rv[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) rv[i] = __ldg(rT + (cc + i) * m);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) dot = __fadd_rn(dot, __fmul_rn(xl[cc + i], rv[i]));
+                }
+                for (; cc < sub; ++cc) dot = __fadd_rn(dot, __fmul_rn(xl[cc], __ldg(rT + cc * m)));
                 c.T[l * 16 + jj] = dot;  // row stride 16 (m <= 16)
             }
         }
@@ -1100,6 +1165,7 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
             __syncwarp();
         }
 
+        PT(0);
         // ---- rounds (routing.cpp:229-240)
         for (uint32_t r = 0; r < P.r_max && !c.overflow; ++r) {
             while (!c.overflow) {
@@ -1107,9 +1173,12 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
                 if (i == EMPTY) break;
                 expand<TFB, EXACT, NCH>(P, c, s, i, lane);
             }
+            PT(2);
             if (r + 1 == P.r_max || !s.end_round(c, lane)) break;
+            PT(7);
         }
         // final flush (routing.cpp:242) and truncation to K (:244-246)
+        PT(2);
         s.flush(c, lane);
         const uint32_t k_out = min(P.K, c.rl_size);
         const Arr res = c.rl_cur_arr();
@@ -1117,6 +1186,7 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
             P.out_ids[static_cast<uint64_t>(qid) * P.K + i] = res.id[i];
             P.out_sq[static_cast<uint64_t>(qid) * P.K + i] = res.sq[i];
         }
+        PT(7);
         if (lane == 0) {
             P.out_n[qid] = k_out;
             uint32_t* st = P.out_stats + static_cast<uint64_t>(qid) * kStatWords;
@@ -1132,6 +1202,10 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
         __syncwarp();
     }
     if (lane == 0) P.slot_epoch[slot] = epoch;
+#ifdef PAG_PHASE_TIMING
+    if (lane == 0)
+        for (int k = 0; k < 8; ++k) atomicAdd(&g_phase[k], static_cast<unsigned long long>(c.pt_acc[k]));
+#endif
 }
 
 template <class TFB, bool EXACT, int NCH>
@@ -1173,6 +1247,19 @@ size_t search_kernel_smem(const SearchLaunch& L) {
 }
 
 bool search_uses_registers(const SearchLaunch& L) { return L.b <= 32; }
+
+void search_phase_cycles(unsigned long long* out8, bool reset) {
+#ifdef PAG_PHASE_TIMING
+    cudaMemcpyFromSymbol(out8, g_phase, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_phase, z, sizeof(z));
+    }
+#else
+    for (int k = 0; k < 8; ++k) out8[k] = 0;
+    (void)reset;
+#endif
+}
 
 cudaError_t search_occupancy(const SearchLaunch& L, int* blocks_per_sm) { return dispatch(L, 0, nullptr, blocks_per_sm); }
 
