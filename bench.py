@@ -192,7 +192,10 @@ def main():
     ap.add_argument("--efs", type=int, default=0, help="fixed efS (default: sweep to recall 0.95)")
     ap.add_argument("--target-recall", type=float, default=0.95)
     ap.add_argument("--cache-dir", default=os.environ.get("PAG_CACHE", "/tmp/pag_b200_cache"))
-    ap.add_argument("--fast-dist", action="store_true", help="warp-tree distances instead of reference order")
+    ap.add_argument("--dist", default="warp-tree", choices=["warp-tree", "exact"],
+                    help="timed distance mode: warp-tree FMA reduction (the north-star design, within "
+                         "1e-5 of the reference) or the reference's own fp32 order (bit-identical); the "
+                         "other mode is also timed and compared")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -233,7 +236,7 @@ def choose_efs(ix, queries, gt_ids, gt_sq, cfg, args, pag):
     for efs in cfg["efs"]:
         if efs < K:
             continue
-        r = ix.search_batch(queries, pag.SearchParams(K=K, efS=efs, exact_dist=not args.fast_dist))
+        r = ix.search_batch(queries, pag.SearchParams(K=K, efS=efs, exact_dist=args.dist == 'exact'))
         rec = pag.mean_recall(r.ids, r.n_out, gt_ids, gt_sq, K)
         st = r.stats.astype(np.float64)
         sweep.append({"efS": efs, "recall": round(rec, 4), "exact": round(float(st[:, 0].mean()), 1),
@@ -279,10 +282,10 @@ def run_pag(args, cfg, paths, rank, world, local_rank, threads, dist):
             efs, sweep = choose_efs(ix, queries, gt_ids, gt_sq, cfg, args, pag)
             with open(os.path.join(os.path.dirname(paths["index"]), "operating_point.json"), "w") as f:
                 json.dump({"efS": efs, "sweep": sweep}, f)
-        r = ix.search_batch(queries, pag.SearchParams(K=K, efS=efs, exact_dist=not args.fast_dist))
+        r = ix.search_batch(queries, pag.SearchParams(K=K, efS=efs, exact_dist=args.dist == 'exact'))
         recall = pag.mean_recall(r.ids, r.n_out, gt_ids, gt_sq, K)
     efs = broadcast_int(efs, dist, dev)  # control plane only
-    params = pag.SearchParams(K=K, efS=efs, exact_dist=not args.fast_dist)
+    params = pag.SearchParams(K=K, efS=efs, exact_dist=args.dist == 'exact')
 
     # device-resident batch
     q_dev = torch.from_numpy(queries).to(dev)
@@ -311,13 +314,44 @@ def run_pag(args, cfg, paths, rank, world, local_rank, threads, dist):
         torch.cuda.synchronize(dev)
     per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     total_ms = ev[0].elapsed_time(ev[-1])
+    stats = st_dev.cpu().numpy().view(np.uint32).astype(np.uint64)
+    ids_main = ids_dev.cpu().numpy().view(np.uint32).copy()
+    sq_main = sq_dev.cpu().numpy().copy()
+    n_main = n_dev.cpu().numpy().view(np.uint32).copy()
+
+    # the other distance mode: timed too, and compared on the full batch
+    other_mode = "exact" if args.dist == "warp-tree" else "warp-tree"
+    oparams = pag.SearchParams(K=K, efS=efs, exact_dist=other_mode == "exact")
+    osteps = max(3, min(args.steps, 5))
+    for _ in range(2):
+        ix.search_device(q_dev.data_ptr(), nq, oparams, ids_dev.data_ptr(), sq_dev.data_ptr(),
+                         n_dev.data_ptr(), st_dev.data_ptr(), stream.cuda_stream)
+    oev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    oev[0].record(stream)
+    for _ in range(osteps):
+        ix.search_device(q_dev.data_ptr(), nq, oparams, ids_dev.data_ptr(), sq_dev.data_ptr(),
+                         n_dev.data_ptr(), st_dev.data_ptr(), stream.cuda_stream)
+    oev[1].record(stream)
+    torch.cuda.synchronize(dev)
+    o_ms = max_over_ranks(oev[0].elapsed_time(oev[1]), dist, dev)
+    ids_o = ids_dev.cpu().numpy().view(np.uint32)
+    sq_o = sq_dev.cpu().numpy()
+    n_o = n_dev.cpu().numpy().view(np.uint32)
+    same_set = np.mean([set(ids_main[i, :n_main[i]].tolist()) == set(ids_o[i, :n_o[i]].tolist())
+                        for i in range(nq)])
+    common = (ids_main == ids_o) & (np.arange(K)[None, :] < np.minimum(n_main, n_o)[:, None])
+    rel = np.abs(sq_main - sq_o) / np.maximum(np.abs(sq_o), 1e-30)
+    other = {"distance_mode": other_mode, "value": round(world * nq * osteps / (o_ms / 1e3), 1),
+             "id_sets_equal_frac": round(float(same_set), 5),
+             "max_rel_sq_diff": float(rel[common].max()) if common.any() else 0.0}
+    if rank == 0:
+        other["recall"] = round(pag.mean_recall(ids_o, n_o, gt_ids, gt_sq, K), 4)
     if dist is not None:
         dist.barrier()
     total_ms = max_over_ranks(total_ms, dist, dev)
     ms_per_step = total_ms / args.steps
     value = world * nq * args.steps / (total_ms / 1e3)
 
-    stats = st_dev.cpu().numpy().view(np.uint32).astype(np.uint64)
     status = int(np.bitwise_or.reduce(stats[:, 5])) if nq else 0
     bytes_total = algorithmic_bytes(stats[:, [0, 1, 2, 3, 4]], ix.padded_dim, ix.L, K)
     kernel_ms = float(np.mean(per_step))
@@ -371,12 +405,13 @@ def run_pag(args, cfg, paths, rank, world, local_rank, threads, dist):
         "data": "synthetic (seeded Gaussian mixture per BASELINE.json; index from the reference CPU build)",
         "config": {"workload": args.config, "n": cfg["n"], "d": cfg["d"], "queries_per_step": nq,
                    "K": K, "efS": efs, "recall": round(recall, 4), "sweep": sweep,
-                   "distance_mode": "warp-tree" if args.fast_dist else "reference-order (bit-exact)",
+                   "distance_mode": args.dist,
+                   "other_mode": other,
                    "l2": "index (>3 GB) exceeds the 126 MB L2; no flush needed",
                    "parallelism": f"query shards, index replica per GPU x{world}"},
         "e2e": {"value": round(e2e_qps, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
-        "gpu_launches": args.steps,
+        "gpu_launches": args.steps,  # one pag_search_kernel launch per step
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind,
                      "bytes_per_query": round(bytes_total / nq, 1)},
