@@ -799,14 +799,17 @@ template <bool EXACT, int NCH>
 __device__ __forceinline__ void distances(const SearchLaunch& P, Common& c, uint32_t items, uint32_t w,
                                           int lane) {
     const IndexView& ix = P.ix;
-    if ((items >> lane) & 1u) {
+    const bool mine = (items >> lane) & 1u;
+    uint32_t deg = 0;
+    if (mine) {
         prefetch_l2_bulk(ix.rows + static_cast<uint64_t>(w) * ix.dstride, ix.dstride * 4u);
-        c.degbuf[lane] = __ldg(ix.deg + w);
+        deg = __ldg(ix.deg + w);  // consumed after the rows: its latency overlaps theirs
     }
     if (EXACT)
         dist_exact<NCH>(P, c, items, w, lane);
     else
         dist_fast<NCH>(P, c, items, w, lane);
+    if (mine) c.degbuf[lane] = deg;
     __syncwarp();
 }
 
