@@ -535,7 +535,7 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     L.off_sqbuf = off;
     off = align16(off + 256);
     L.off_stage = off;
-    off = align16(off + 4 * 36 * 16);
+    if (p.exact_dist) off = align16(off + 4 * 36 * 16);  // transposed chain staging (exact mode only)
     // movable regions: W (12b), rings (24b), R_L (24 capr), merge (48b);
     // with b <= 32 the working set and rings live in registers
     const uint64_t szW = regs ? 0 : align16(12 * b), szR = regs ? 0 : align16(24 * b),

@@ -864,6 +864,20 @@ __device__ __forceinline__ void prefetch_block(const IndexView& ix, uint32_t u, 
     prefetch_l2_bulk(blk + 16u * S, 4u * ix.cwp * deg);
 }
 
+// warp-parallel variant: lane i prefetches one 128-B line of the used part of
+// the block (4 scalar arrays, then the codes), one instruction for the warp
+__device__ __forceinline__ void prefetch_block_lanes(const IndexView& ix, uint32_t u, uint32_t deg, int lane) {
+    const uint8_t* blk = ix.adj + static_cast<uint64_t>(u) * ix.block_bytes;
+    const uint32_t S = ix.slot_stride;
+    const uint32_t lines_scalar = (4u * deg + 127u) / 128u;            // per scalar array
+    const uint32_t lines_codes = (4u * ix.cwp * deg + 127u) / 128u;
+    const uint32_t li = static_cast<uint32_t>(lane);
+    const uint8_t* p = nullptr;
+    if (li < 4u * lines_scalar) p = blk + (li / lines_scalar) * 4u * S + (li % lines_scalar) * 128u;
+    else if (li < 4u * lines_scalar + lines_codes) p = blk + 16u * S + (li - 4u * lines_scalar) * 128u;
+    if (p && deg) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // routing.cpp:139-204 for W slot `slot`
 template <class TFB, bool EXACT, int NCH>
 __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, int lane) {
@@ -987,6 +1001,7 @@ __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
                 // an admitted node is usually expanded later: start its
                 // adjacency on the way to L2 now (hides the next dependency)
                 if ((P.tune & 1u) && lane == 0) prefetch_block(ix, w_j, deg_j);
+                if (P.tune & 16u) prefetch_block_lanes(ix, w_j, deg_j, lane);
             } else {
                 s.push_fp(w_j, sq_j, deg_j, lane);
             }
