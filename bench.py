@@ -226,7 +226,86 @@ def main():
     if args.impl == "reference":
         run_reference(args, cfg, paths, rank, world, threads, dist)
         return
+    if args.config == "cfg5":
+        if rank == 0:
+            run_online(args, cfg, paths, threads)
+        return
     run_pag(args, cfg, paths, rank, world, local_rank, threads, dist)
+
+
+def run_online(args, cfg, paths, threads):
+    """Config 5: the reference applies 20 insert_online batches (one process,
+    one PesSet, like insert-bench pag_cli.cpp:327-366) and saves the index
+    after each; the GPU refreshes in place from each phase file (only new rows
+    and changed node blocks travel), recomputes exact ground truth against
+    the current contents and times the 10k-query batch at the efS that gave
+    recall 0.95 in phase 0."""
+    import torch
+
+    import paper_2603_06660_b200 as pag
+
+    K = cfg["K"]
+    ins_path = os.path.join(os.path.dirname(paths["index"]), "inserts.fvecs")
+    if not os.path.exists(ins_path):
+        write_fvecs(ins_path, gaussian_mixture(cfg["inserts"], cfg["d"], cfg["centres"], cfg["sigma"], seed=3,
+                                               centre_seed=SEEDS["centre"], unit=cfg["unit"]))
+    queries = read_fvecs(paths["queries"])
+    nq = queries.shape[0]
+    ix = pag.load_index(paths["index"])
+    gt_ids, gt_sq = ix.ground_truth(queries, K)
+    efs, sweep = args.efs, []
+    if not efs:
+        efs, sweep = choose_efs(ix, queries, gt_ids, gt_sq, cfg, args, pag)
+    params = pag.SearchParams(K=K, efS=efs, exact_dist=args.dist == "exact")
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.Stream(dev)
+    q_dev = torch.from_numpy(queries).to(dev)
+    outs = [torch.empty((nq, K), dtype=torch.int32, device=dev), torch.empty((nq, K), dtype=torch.float32, device=dev),
+            torch.empty((nq,), dtype=torch.int32, device=dev), torch.empty((nq, 8), dtype=torch.int32, device=dev)]
+
+    def timed_qps():
+        for _ in range(3):
+            ix.search_device(q_dev.data_ptr(), nq, params, *(t.data_ptr() for t in outs), stream.cuda_stream)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record(stream)
+        for _ in range(args.steps):
+            ix.search_device(q_dev.data_ptr(), nq, params, *(t.data_ptr() for t in outs), stream.cuda_stream)
+        ev[1].record(stream)
+        torch.cuda.synchronize(dev)
+        return nq * args.steps / (ev[0].elapsed_time(ev[1]) / 1e3)
+
+    phases = [{"phase": "base", "n_indexed": ix.n, "qps": round(timed_qps(), 1),
+               "recall": round(pag.mean_recall(outs[0].cpu().numpy().view(np.uint32),
+                                               outs[2].cpu().numpy().view(np.uint32), gt_ids, gt_sq, K), 4)}]
+    prefix = os.path.join(os.path.dirname(paths["index"]), "phase")
+    proc = subprocess.Popen([REF_BIN, "insert", f"--index={paths['index']}", f"--data={ins_path}",
+                             f"--batches={cfg['batches']}", f"--out-prefix={prefix}"],
+                            stdout=subprocess.PIPE, text=True)
+    for b in range(cfg["batches"]):
+        line = json.loads(proc.stdout.readline())  # the reference finished batch b
+        st = ix.refresh(line["path"])
+        t = time.time()
+        gt_ids, gt_sq = ix.ground_truth(queries, K)
+        gt_s = time.time() - t
+        qps = timed_qps()
+        rec = pag.mean_recall(outs[0].cpu().numpy().view(np.uint32), outs[2].cpu().numpy().view(np.uint32),
+                              gt_ids, gt_sq, K)
+        phases.append({"phase": b, "n_indexed": ix.n, "reference_insert_s": line["insert_seconds"],
+                       "refresh_s": round(st["seconds"], 4), "changed_blocks": st["changed_blocks"],
+                       "bytes_uploaded": st["bytes_uploaded"], "gt_s": round(gt_s, 3), "qps": round(qps, 1),
+                       "recall": round(rec, 4)})
+        log(f"phase {b}: n={ix.n} refresh {st['seconds']:.3f}s ({st['changed_blocks']} blocks) "
+            f"qps {qps:.0f} recall {rec:.4f}")
+        if b + 1 < cfg["batches"]:
+            os.remove(line["path"])
+    proc.wait()
+    print(json.dumps({"metric": f"QPS and recall@{K} per phase under online insertion (config 5)",
+                      "value": round(float(np.mean([p["qps"] for p in phases])), 1), "unit": "queries/s",
+                      "n_gpus": 1, "steps": args.steps, "higher_is_better": True, "dtype": "f32",
+                      "config": {"workload": "cfg5", "n0": cfg["n"], "inserts": cfg["inserts"],
+                                 "batches": cfg["batches"], "K": K, "efS": efs, "sweep": sweep,
+                                 "distance_mode": args.dist},
+                      "phases": phases}), flush=True)
 
 
 def choose_efs(ix, queries, gt_ids, gt_sq, cfg, args, pag):

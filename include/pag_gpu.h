@@ -113,6 +113,15 @@ int pag_gpu_search_device(pag_gpu_index* ix, const float* q_dev, uint64_t nq,
 int pag_gpu_ground_truth(pag_gpu_index* ix, const float* queries, uint64_t nq, uint32_t k,
                          uint32_t* ids, float* sq);
 
+/* Online-insert refresh: re-synchronise the
+ * resident index with a newer PAGIDX01 file the reference saved after
+ * appending nodes (insert_online, proj/src/builder.cpp:354-363; adjacency
+ * rewiring :92-139, PES flush :250-279). The file must extend the loaded one
+ * (same header parameters and entry nodes, n_new >= n). Only new rows/norms
+ * and node blocks whose contents changed are uploaded. stats (may be NULL):
+ * {new nodes, changed node blocks, bytes uploaded, microseconds}. */
+int pag_gpu_refresh(pag_gpu_index* ix, const char* index_path, uint64_t* stats);
+
 /* Host-only: parse and validate a PAGIDX01 file exactly as pag_gpu_open
  * does (same errors), without touching a GPU; fills info[0..9] as
  * pag_gpu_info (n_devices and device bytes are 0). */

@@ -269,6 +269,36 @@ int cmd_tables(const Args& a) {
     return 0;
 }
 
+int cmd_insert(const Args& a) {
+    // online insertion phases (the insert-bench loop, pag_cli.cpp:327-366):
+    // one PesSet across batches; after each batch the index is saved as
+    // <out-prefix>.<b>.pagidx (written to a temp name, then renamed) so a
+    // reader can refresh from it while the next batch is being inserted.
+    PagIndex index = load_index(a.get("index"));
+    uint32_t d;
+    size_t n_ins;
+    std::vector<float> xs = read_fvecs_raw(a.get("data"), &d, &n_ins);
+    if (d != index.vectors().dim()) throw std::runtime_error("insert dimension mismatch");
+    const uint32_t batches = std::stoul(a.get("batches", "1"));
+    const size_t per_batch = n_ins / batches;
+    const std::string prefix = a.get("out-prefix");
+    index.reserve(index.size() + per_batch * batches);
+    PesSet pes;
+    for (uint32_t b = 0; b < batches; ++b) {
+        auto t0 = clk::now();
+        for (size_t i = b * per_batch; i < (b + 1) * per_batch; ++i)
+            insert_online(index, std::span<const float>(xs.data() + i * d, d), pes);
+        const double ins_s = std::chrono::duration<double>(clk::now() - t0).count();
+        const std::string path = prefix + "." + std::to_string(b) + ".pagidx";
+        save_index(index, path + ".tmp");
+        std::rename((path + ".tmp").c_str(), path.c_str());
+        std::printf("{\"batch\": %u, \"n_indexed\": %u, \"insert_seconds\": %.3f, \"path\": \"%s\"}\n", b,
+                    index.size(), ins_s, path.c_str());
+        std::fflush(stdout);
+    }
+    return 0;
+}
+
 int cmd_sqdist(const Args& a) {
     // sq_dist of query rows against listed base rows, for the distance KATs
     PagIndex index = load_index(a.get("index"));
@@ -295,7 +325,7 @@ int cmd_sqdist(const Args& a) {
 int main(int argc, char** argv) {
     if (argc < 2) {
         std::fprintf(stderr,
-                     "usage: pag_ref {gen-synthetic|build|search|gt|refs|tables|sqdist} "
+                     "usage: pag_ref {gen-synthetic|build|search|gt|refs|tables|sqdist|insert} "
                      "--key=value ...\n");
         return 2;
     }
@@ -309,6 +339,7 @@ int main(int argc, char** argv) {
         if (cmd == "refs") return cmd_refs(a);
         if (cmd == "tables") return cmd_tables(a);
         if (cmd == "sqdist") return cmd_sqdist(a);
+        if (cmd == "insert") return cmd_insert(a);
     } catch (const std::exception& e) {
         std::fprintf(stderr, "error: %s\n", e.what());
         return 1;

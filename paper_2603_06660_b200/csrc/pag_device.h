@@ -128,6 +128,10 @@ struct GtTcLaunch {
     uint32_t* uncertified;    // nq flags: 1 = re-run exactly
 };
 cudaError_t launch_gt_tc(const GtTcLaunch& g, cudaStream_t stream);
+
+// pag_util.cu: staged node blocks -> their slots in the adjacency array
+cudaError_t scatter_blocks(const void* staging, const uint32_t* ids, uint32_t count, void* adj,
+                           uint32_t block_bytes, cudaStream_t stream);
 size_t gt_tc_smem_bytes();
 uint32_t gt_tc_cmax();
 uint32_t gt_tc_block_n();

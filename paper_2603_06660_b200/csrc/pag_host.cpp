@@ -15,6 +15,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -168,6 +169,7 @@ struct Replica {
     float* refsT = nullptr;
     uint32_t* entries = nullptr;
     float* bnorm = nullptr;  // squared row norms (from the file's cached norms), GT only
+    uint64_t cap_nodes = 0;  // allocated node capacity (refresh grows it)
     size_t bytes = 0;
     // search scratch
     uint64_t* gtab = nullptr;
@@ -217,6 +219,9 @@ struct pag_gpu_index {
     uint64_t total_edges = 0;
     float max_bnorm = 0.0f;        // max squared row norm
     uint64_t gt_uncertified = 0;   // tensor-core GT queries re-run exactly (diagnostic)
+    // host mirror of the device adjacency + degrees (built at the first refresh)
+    std::vector<uint8_t> mirror_adj;
+    std::vector<uint32_t> mirror_deg;
     std::vector<float> refs;
     std::vector<Replica> reps;
     std::mutex mu;
@@ -257,6 +262,27 @@ void free_replica(Replica& r) {
     if (r.h_pin) cudaFreeHost(r.h_pin);
     if (r.stream) cudaStreamDestroy(r.stream);
     r = Replica{};
+}
+
+// One node's file records {target u32, codes[cb], cos_beta, edge_norm,
+// base_offset} (builder.cpp:418-425) -> the device block (zeroed by caller).
+void fill_block(uint8_t* blk, const uint8_t* e, uint32_t deg, uint64_t n, uint32_t S, uint32_t cb, uint32_t cwp) {
+    const size_t rec = 4 + cb + 12;
+    uint32_t* tg = reinterpret_cast<uint32_t*>(blk);
+    float* en = reinterpret_cast<float*>(blk + 4u * S);
+    float* cbeta = reinterpret_cast<float*>(blk + 8u * S);
+    float* bo = reinterpret_cast<float*>(blk + 12u * S);
+    uint8_t* codes = blk + 16u * S;
+    for (uint32_t j = 0; j < deg; ++j, e += rec) {
+        uint32_t t;
+        std::memcpy(&t, e, 4);
+        if (t >= n) throw_err(PAG_GPU_ERUNTIME, "edge target out of range in file");
+        tg[j] = t;
+        std::memcpy(codes + static_cast<size_t>(j) * 4 * cwp, e + 4, cb);
+        std::memcpy(&cbeta[j], e + 4 + cb, 4);
+        std::memcpy(&en[j], e + 8 + cb, 4);
+        std::memcpy(&bo[j], e + 12 + cb, 4);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -339,6 +365,7 @@ std::unique_ptr<pag_gpu_index> open_index(const char* path, uint32_t device_mask
         dev_alloc(&r.qcounter, 16);
         r.bytes = n * row_bytes + 4ull * n + static_cast<size_t>(n) * ix->block_bytes +
                   4ull * ix->refs.size();
+        r.cap_nodes = n;
         ix->reps.push_back(r);
     }
 
@@ -408,23 +435,7 @@ std::unique_ptr<pag_gpu_index> open_index(const char* path, uint32_t device_mask
             if (deg > ix->maxdeg) throw_err(PAG_GPU_ERUNTIME, "degree over cap in file");
             dg[i] = deg;
             ix->total_edges += deg;
-            const uint8_t* e = cur.take(rec * deg);
-            uint8_t* blk = blk0 + i * ix->block_bytes;
-            uint32_t* tg = reinterpret_cast<uint32_t*>(blk);
-            float* en = reinterpret_cast<float*>(blk + 4u * S);
-            float* cbeta = reinterpret_cast<float*>(blk + 8u * S);
-            float* bo = reinterpret_cast<float*>(blk + 12u * S);
-            uint8_t* codes = blk + 16u * S;
-            for (uint32_t j = 0; j < deg; ++j, e += rec) {
-                uint32_t t;
-                std::memcpy(&t, e, 4);
-                if (t >= n) throw_err(PAG_GPU_ERUNTIME, "edge target out of range in file");
-                tg[j] = t;
-                std::memcpy(codes + static_cast<size_t>(j) * 4 * cwp, e + 4, cb);
-                std::memcpy(&cbeta[j], e + 4 + cb, 4);
-                std::memcpy(&en[j], e + 8 + cb, 4);
-                std::memcpy(&bo[j], e + 12 + cb, 4);
-            }
+            fill_block(blk0 + i * ix->block_bytes, cur.take(rec * deg), deg, n, S, cb, cwp);
         }
         for (auto& r : ix->reps) {
             cudaSetDevice(r.device);
@@ -830,6 +841,139 @@ void ground_truth_on_replica(pag_gpu_index& ix, Replica& r, const float* q, uint
     }
 }
 
+// Online-insert refresh: the reference appended
+// rows (insert_online, builder.cpp:354-363) and rewired adjacency lists
+// (rebuild_neighbors :92-124, append_edge :126-139, PES flush :250-279) and
+// saved the index again. Only what changed travels: new rows and norms, and
+// the node blocks whose bytes differ from the host mirror, scattered on the
+// device by one kernel. stats: {new nodes, dirty blocks, bytes uploaded, us}.
+void grow_replica(pag_gpu_index& ix, Replica& r, uint64_t need) {
+    if (need <= r.cap_nodes) return;
+    const uint64_t cap = std::max<uint64_t>(need, r.cap_nodes + r.cap_nodes / 4 + 1024);
+    const size_t row_bytes = 4ull * ix.dstride;
+    auto regrow = [&](auto** p, size_t old_bytes, size_t new_bytes) {
+        void* q = nullptr;
+        cuda_check(cudaMalloc(&q, new_bytes), "cudaMalloc");
+        if (*p && old_bytes) cuda_check(cudaMemcpy(q, *p, old_bytes, cudaMemcpyDeviceToDevice), "D2D grow");
+        dev_free(*p);
+        *p = static_cast<std::remove_reference_t<decltype(**p)>*>(q);
+    };
+    regrow(&r.rows, ix.n * row_bytes, cap * row_bytes);
+    regrow(&r.deg, ix.n * 4, cap * 4);
+    regrow(&r.adj, ix.n * ix.block_bytes, cap * ix.block_bytes);
+    regrow(&r.bnorm, ix.n * 4, cap * 4);
+    r.cap_nodes = cap;
+}
+
+void refresh_index(pag_gpu_index& ix, const char* path, uint64_t* st) {
+    const auto t0 = std::chrono::steady_clock::now();
+    Mapped mp;
+    mp.fd = ::open(path, O_RDONLY);
+    if (mp.fd < 0) throw_err(PAG_GPU_ERUNTIME, std::string("cannot open index: ") + path);
+    struct stat sb;
+    if (fstat(mp.fd, &sb) != 0 || sb.st_size == 0) throw_err(PAG_GPU_ERUNTIME, "index read failed");
+    mp.size = static_cast<size_t>(sb.st_size);
+    void* mm = mmap(nullptr, mp.size, PROT_READ, MAP_PRIVATE, mp.fd, 0);
+    if (mm == MAP_FAILED) throw_err(PAG_GPU_ERUNTIME, std::string("cannot open index: ") + path);
+    mp.p = static_cast<const uint8_t*>(mm);
+    Cursor cur{mp.p, mp.size};
+    if (cur.pod<uint64_t>() != 0x5041474944583031ull) throw_err(PAG_GPU_ERUNTIME, "bad index magic");
+    if (cur.pod<uint32_t>() != 1u) throw_err(PAG_GPU_ERUNTIME, "unsupported index version");
+    const uint64_t n_new = cur.pod<uint64_t>();
+    const uint32_t dim = cur.pod<uint32_t>(), padded = cur.pod<uint32_t>(), L = cur.pod<uint32_t>(),
+                   m = cur.pod<uint32_t>(), M = cur.pod<uint32_t>();
+    cur.pod<uint32_t>();  // efC
+    cur.pod<uint32_t>();  // b_build
+    cur.pod<uint32_t>();  // pes_flush_interval
+    const uint64_t seed = cur.pod<uint64_t>();
+    const uint8_t metric = cur.pod<uint8_t>();
+    cur.pod<uint8_t>();
+    const uint32_t ne = cur.pod<uint32_t>();
+    const uint8_t* ent = cur.take(4ull * ne);
+    if (dim != ix.dim || padded != ix.padded || (L != ix.L && L != 0) || m != ix.m || M != ix.M ||
+        seed != ix.seed || metric != ix.metric || n_new < ix.n || ne != ix.entries.size() ||
+        (ne && std::memcmp(ent, ix.entries.data(), 4ull * ne) != 0))
+        throw_err(PAG_GPU_EINVAL, "refresh: index is not an extension of the loaded one");
+    const uint64_t n_old = ix.n;
+    const uint32_t BB = ix.block_bytes, S = ix.slot_stride, cb = ix.cb, cwp = ix.cwp;
+    const size_t rec = 4 + cb + 12;
+    Replica& r0 = ix.reps.at(0);
+    cudaSetDevice(r0.device);
+    if (ix.mirror_deg.size() != n_old) {  // first refresh: mirror the device state
+        ix.mirror_adj.resize(n_old * BB);
+        ix.mirror_deg.resize(n_old);
+        cuda_check(cudaMemcpy(ix.mirror_adj.data(), r0.adj, n_old * BB, cudaMemcpyDeviceToHost), "D2H mirror");
+        cuda_check(cudaMemcpy(ix.mirror_deg.data(), r0.deg, 4 * n_old, cudaMemcpyDeviceToHost), "D2H mirror");
+    }
+    ix.mirror_adj.resize(n_new * BB);
+    ix.mirror_deg.resize(n_new);
+    std::vector<uint32_t> dirty;
+    std::vector<uint8_t> blk(BB);
+    uint64_t edges = 0;
+    for (uint64_t u = 0; u < n_new; ++u) {
+        const uint32_t deg = cur.pod<uint32_t>();
+        if (deg > ix.maxdeg) throw_err(PAG_GPU_ERUNTIME, "degree over cap in file");
+        edges += deg;
+        std::fill(blk.begin(), blk.end(), 0);
+        fill_block(blk.data(), cur.take(rec * deg), deg, n_new, S, cb, cwp);
+        uint8_t* mb = &ix.mirror_adj[u * BB];
+        if (u >= n_old || ix.mirror_deg[u] != deg || std::memcmp(mb, blk.data(), BB) != 0) {
+            std::memcpy(mb, blk.data(), BB);
+            ix.mirror_deg[u] = deg;
+            dirty.push_back(static_cast<uint32_t>(u));
+        }
+    }
+    const uint8_t* rows = cur.take(4ull * padded * n_new);
+    const uint8_t* norms = cur.take(4ull * n_new);
+    const size_t row_bytes = 4ull * ix.dstride;
+    std::vector<uint8_t> newrows((n_new - n_old) * row_bytes, 0);
+    std::vector<float> newbn(n_new - n_old);
+    for (uint64_t i = n_old; i < n_new; ++i) {
+        std::memcpy(&newrows[(i - n_old) * row_bytes], rows + i * 4ull * padded, 4ull * padded);
+        float v;
+        std::memcpy(&v, norms + 4 * i, 4);
+        newbn[i - n_old] = v * v;
+        ix.max_bnorm = std::max(ix.max_bnorm, newbn[i - n_old]);
+    }
+    std::vector<uint8_t> staging(dirty.size() * BB);
+    for (size_t i = 0; i < dirty.size(); ++i)
+        std::memcpy(&staging[i * BB], &ix.mirror_adj[static_cast<uint64_t>(dirty[i]) * BB], BB);
+    uint64_t up = 0;
+    for (auto& r : ix.reps) {
+        cuda_check(cudaSetDevice(r.device), "cudaSetDevice");
+        grow_replica(ix, r, n_new);
+        DevBuf dst(staging.size()), did(4 * dirty.size());
+        if (!dirty.empty()) {
+            cuda_check(cudaMemcpy(dst.p, staging.data(), staging.size(), cudaMemcpyHostToDevice), "H2D blocks");
+            cuda_check(cudaMemcpy(did.p, dirty.data(), 4 * dirty.size(), cudaMemcpyHostToDevice), "H2D ids");
+            cuda_check(pagdev::scatter_blocks(dst.p, did.as<uint32_t>(), static_cast<uint32_t>(dirty.size()), r.adj,
+                                              BB, r.stream),
+                       "scatter blocks");
+        }
+        cuda_check(cudaMemcpyAsync(r.deg, ix.mirror_deg.data(), 4 * n_new, cudaMemcpyHostToDevice, r.stream), "H2D deg");
+        if (n_new > n_old) {
+            cuda_check(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(r.rows) + n_old * row_bytes, newrows.data(),
+                                       newrows.size(), cudaMemcpyHostToDevice, r.stream),
+                       "H2D rows");
+            cuda_check(cudaMemcpyAsync(r.bnorm + n_old, newbn.data(), 4 * newbn.size(), cudaMemcpyHostToDevice,
+                                       r.stream),
+                       "H2D norms");
+        }
+        cuda_check(cudaStreamSynchronize(r.stream), "refresh");
+        r.bytes = r.cap_nodes * (row_bytes + 4 + BB) + 4ull * ix.refs.size();
+        up = staging.size() + 4 * dirty.size() + 4 * n_new + newrows.size() + 4 * newbn.size();
+    }
+    ix.n = n_new;
+    ix.total_edges = edges;
+    if (st) {
+        st[0] = n_new - n_old;
+        st[1] = dirty.size();
+        st[2] = up;
+        st[3] = static_cast<uint64_t>(
+            std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+    }
+}
+
 template <typename F>
 int guarded(F&& f) {
     try {
@@ -890,6 +1034,14 @@ int pag_gpu_reference_family(uint32_t padded_dim, uint32_t L, uint32_t m, uint64
 }
 
 uint32_t pag_gpu_default_subspace_count(uint32_t dim) { return default_L(dim); }
+
+int pag_gpu_refresh(pag_gpu_index* ix, const char* index_path, uint64_t* stats) {
+    return guarded([&] {
+        if (!ix || !index_path) throw_err(PAG_GPU_EINVAL, "null argument");
+        std::lock_guard<std::mutex> g(ix->mu);
+        refresh_index(*ix, index_path, stats);
+    });
+}
 
 int pag_gpu_close(pag_gpu_index* ix) {
     return guarded([&] {

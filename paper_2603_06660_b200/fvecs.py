@@ -77,4 +77,8 @@ CONFIGS = {
                  efs=[100, 200, 300, 500, 800, 1000, 2000]),
     "cfg4": dict(n=2_000_000, d=512, centres=8192, sigma=0.4, unit=True, nq=20_000, K=1000,
                  efs=[1000, 2000, 3000, 4000]),
+    # online insertion: config-1 distribution, 800k indexed, 200k inserts in
+    # 20 batches interleaved with 10k-query batches (insert-bench shape)
+    "cfg5": dict(n=800_000, d=128, centres=100, sigma=0.5, unit=False, nq=10_000, K=10,
+                 efs=[10, 20, 30, 40, 60, 80, 100, 150, 200], inserts=200_000, batches=20),
 }

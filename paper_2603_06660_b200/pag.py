@@ -152,6 +152,24 @@ class PagIndex:
         check(lib.pag_gpu_search_device(self._h, q_ptr, nq, C.byref(pc), ids_ptr, sq_ptr,
                                         n_out_ptr, stats_ptr, stream or None))
 
+    def refresh(self, path: str) -> dict:
+        """Re-synchronise with a newer file of the same index (online inserts
+        applied by the reference); uploads only what changed."""
+        st = np.zeros(4, np.uint64)
+        check(lib.pag_gpu_refresh(self._h, path.encode(), st))
+        info = np.zeros(12, np.uint64)
+        check(lib.pag_gpu_info(self._h, info, 12))
+        self.n, self.total_edges, self.device_bytes = int(info[0]), int(info[9]), int(info[11])
+        self.path = path
+        return {"new_nodes": int(st[0]), "changed_blocks": int(st[1]), "bytes_uploaded": int(st[2]),
+                "seconds": int(st[3]) / 1e6}
+
+    def gt_uncertified(self) -> int:
+        """Tensor-core ground-truth queries that failed the certificate and were re-run exactly."""
+        info = np.zeros(13, np.uint64)
+        check(lib.pag_gpu_info(self._h, info, 13))
+        return int(info[12])
+
     def ground_truth(self, queries: np.ndarray, k: int) -> Tuple[np.ndarray, np.ndarray]:
         """bench.cpp:18-53 over the resident base rows: top-min(k, n) by (sq, id)."""
         q = np.ascontiguousarray(queries, np.float32).reshape(-1, self.dim)

@@ -1,0 +1,59 @@
+"""Online-insert refresh (BASELINE config 5 shape):
+the unmodified reference applies insert_online batches (oracle/_ref/pag_ref
+insert, one PesSet across batches like insert-bench) and saves the index
+after each; the GPU index is refreshed in place from each phase file and must
+search exactly like the oracle on that file."""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import assert_same_results
+from oracle import oracle as O
+from paper_2603_06660_b200.fvecs import gaussian_mixture, write_fvecs
+
+
+@pytest.fixture(scope="module")
+def phases(fixture_dir):
+    if not O.have_ref():
+        pytest.skip("oracle/_ref/pag_ref not built")
+    base = gaussian_mixture(1500, 32, 12, 0.5, seed=41, centre_seed=7)
+    ins = gaussian_mixture(450, 32, 12, 0.5, seed=42, centre_seed=7)
+    q = gaussian_mixture(40, 32, 12, 0.5, seed=43, centre_seed=7)
+    b, i, idx = (os.path.join(fixture_dir, f) for f in ("rf_base.fvecs", "rf_ins.fvecs", "rf.pagidx"))
+    write_fvecs(b, base)
+    write_fvecs(i, ins)
+    O.ref_build(b, idx, threads=1, M=8, efC=60, seed=5)
+    prefix = os.path.join(fixture_dir, "rf_phase")
+    O.ref_run("insert", index=idx, data=i, batches=3, **{"out-prefix": prefix})
+    return idx, [f"{prefix}.{k}.pagidx" for k in range(3)], q
+
+
+def test_phase_files_extend_the_base(phases):
+    idx, files, _ = phases
+    sizes = [O.OracleIndex(p).n for p in [idx] + files]
+    assert sizes == [1500, 1650, 1800, 1950]
+
+
+@pytest.mark.gpu
+def test_refresh_matches_oracle_each_phase(phases):
+    import paper_2603_06660_b200 as pag
+    idx, files, q = phases
+    ix = pag.load_index(idx)
+    try:
+        for path in files:
+            st = ix.refresh(path)
+            assert st["new_nodes"] == 150 and 150 <= st["changed_blocks"] < ix.n
+            for K, efS in ((10, 40), (20, 80)):
+                got = ix.search_batch(q, pag.SearchParams(K=K, efS=efS))
+                want = O.OracleIndex(path).search(q, K, efS)
+                assert_same_results((got.ids, got.sq, got.n_out, got.stats), want, path)
+            gi, gs = ix.ground_truth(q, 10)
+            oi, os_ = O.ground_truth(O.OracleIndex(path).rows(), q, 10)
+            assert np.array_equal(gi, oi)
+        with pytest.raises(ValueError, match="not an extension"):
+            ix.refresh(idx)  # shrinking is refused
+    finally:
+        ix.close()
