@@ -76,7 +76,7 @@ struct SearchLaunch {
     uint32_t off_stage, stage_rows;
     uint32_t off_W, W_in_smem;
     uint32_t off_rf, off_rt, rings_in_smem;
-    uint32_t off_rl, rl_in_smem;
+    uint32_t off_rl, rl_in_smem, rl_cap;  // R_L append buffer (+ sort scratch)
     uint32_t off_merge, merge_in_smem;
     uint32_t warps_per_block;
     uint32_t tune;  // experiment bits (PAG_GPU_TUNE): 1 admit-time adjacency prefetch, 2 next-node prefetch

@@ -533,7 +533,9 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     L.stage_rows = 4;
     L.hash_log2 = p.efS <= 200 ? 10 : 11;
     if (const char* e = std::getenv("PAG_GPU_HASH_LOG2")) L.hash_log2 = static_cast<uint32_t>(std::atoi(e));
-    const uint32_t b = L.b, capr = std::max(1u, p.efS);
+    const uint32_t b = L.b;
+    L.rl_cap = L.r_max * b + b;  // every W flush of a query (r_max - 1 end_rounds + the final flush)
+    const uint32_t capr = L.rl_cap;
     const bool regs = pagdev::search_uses_registers(L);
     // fixed smem regions
     uint32_t off = 0;

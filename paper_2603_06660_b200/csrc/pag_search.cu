@@ -111,16 +111,18 @@ struct Common {
     uint32_t gt_log2, gt_count, epoch;
     bool gt_used, overflow;
     // R_L double buffer (cap efS) and a scratch array (cap 2b)
-    Arr rlA, rlB, mo;
-    uint32_t rl_cur, rl_size, cap_r;
+    // R_L (routing.hpp:150, capacity efS) is never read during the search:
+    // flushed W entries are appended here and the cap-limited sorted list is
+    // formed once at the end (the bounded insert keeps the efS smallest, an
+    // order-independent result). rl_tmp is the final sort's scratch.
+    Arr rl, rl_tmp, mo;
+    uint32_t rl_size, cap_r;
     // counters (routing.hpp:24-34 + edges_scanned)
     uint32_t n_exact, n_test, n_pass, n_visited, n_edges;
 #ifdef PAG_PHASE_TIMING
     long long pt_t0, pt_acc[8];
 #endif
 
-    __device__ Arr rl_cur_arr() const { return rl_cur ? rlB : rlA; }
-    __device__ Arr rl_next_arr() const { return rl_cur ? rlA : rlB; }
 };
 
 __device__ __forceinline__ bool marked(const Common& c, uint32_t id) {
@@ -207,47 +209,77 @@ __device__ __forceinline__ uint32_t count_less(const Arr& a, uint32_t n, float v
     return lo;
 }
 
-// routing.cpp:82-90 applied to a sorted batch: R_L keeps the cap_r smallest
-// (the bounded sorted insert is order-independent for distinct ids).
-__device__ void rl_merge(Common& c, const Arr& batch, uint32_t nb, int lane) {
-    if (nb == 0) return;
-    const Arr cur = c.rl_cur_arr(), nxt = c.rl_next_arr();
-    const uint32_t cap = c.cap_r;
-    for (uint32_t i = lane; i < c.rl_size; i += 32) {
-        const float v = cur.sq[i];
-        const uint32_t id = cur.id[i];
-        const uint32_t pos = i + count_less(batch, nb, v, id);
-        if (pos < cap) {
-            nxt.id[pos] = id;
-            nxt.sq[pos] = v;
-        }
+// routing.cpp:82-90: R_L receives flushed W entries (distinct ids); they are
+// appended and the capacity-limited sorted list is formed at the end.
+__device__ __forceinline__ void rl_append(Common& c, uint32_t id, float sq, bool valid, uint32_t offset) {
+    if (valid) {
+        c.rl.id[c.rl_size + offset] = id;
+        c.rl.sq[c.rl_size + offset] = sq;
     }
-    for (uint32_t j = lane; j < nb; j += 32) {
-        const float v = batch.sq[j];
-        const uint32_t id = batch.id[j];
-        const uint32_t pos = j + count_less(cur, c.rl_size, v, id);
-        if (pos < cap) {
-            nxt.id[pos] = id;
-            nxt.sq[pos] = v;
-        }
-    }
-    __syncwarp();
-    c.rl_size = min(cap, c.rl_size + nb);
-    c.rl_cur ^= 1;
 }
 
-// rank sort of n array entries (distinct ids => strict total order)
-__device__ void rank_sort(const Arr& in, const Arr& out, uint32_t n, int lane) {
-    for (uint32_t i = lane; i < n; i += 32) {
-        const float v = in.sq[i];
-        const uint32_t id = in.id[i];
-        uint32_t r = 0;
-        for (uint32_t j = 0; j < n; ++j) r += cless(in.sq[j], in.id[j], v, id) ? 1u : 0u;
-        out.id[r] = id;
-        out.sq[r] = v;
-        out.aux[r] = in.aux[i];
+// warp bitonic sort of 32 (sq, id, aux) tuples, one per lane, ascending
+__device__ __forceinline__ void bitonic32(float& s, uint32_t& id, uint32_t& ax, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const float ps = __shfl_xor_sync(FULL, s, j);
+            const uint32_t pid = __shfl_xor_sync(FULL, id, j);
+            const uint32_t pax = __shfl_xor_sync(FULL, ax, j);
+            const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+            const bool pless = cless(ps, pid, s, id);
+            if (lower == up ? pless : !pless) {
+                s = ps;
+                id = pid;
+                ax = pax;
+            }
+        }
+    }
+}
+
+// Sort n entries of `a` ascending by (sq, id) (distinct ids): 32-element
+// bitonic runs in registers, then merge passes where every element finds its
+// output slot by a binary search of the partner run. `t` is scratch of the
+// same capacity; returns whichever of a / t holds the result.
+__device__ Arr warp_sort(Arr a, Arr t, uint32_t n, int lane) {
+    for (uint32_t base = 0; base < n; base += 32) {
+        const uint32_t i = base + lane;
+        const bool v = i < n;
+        float s = v ? a.sq[i] : CUDART_INF_F;
+        uint32_t id = v ? a.id[i] : EMPTY, ax = v ? a.aux[i] : 0u;
+        bitonic32(s, id, ax, lane);
+        if (v) {
+            a.sq[i] = s;
+            a.id[i] = id;
+            a.aux[i] = ax;
+        }
     }
     __syncwarp();
+    Arr src = a, dst = t;
+    for (uint32_t w = 32; w < n; w <<= 1) {
+        for (uint32_t i = lane; i < n; i += 32) {
+            const uint32_t start = i & ~(w - 1), pstart = start ^ w;
+            const float s = src.sq[i];
+            const uint32_t id = src.id[i], ax = src.aux[i];
+            uint32_t out = i;
+            if (pstart < n) {
+                Arr p;
+                p.id = src.id + pstart;
+                p.sq = src.sq + pstart;
+                p.aux = src.aux + pstart;
+                out = min(start, pstart) + (i - start) + count_less(p, min(w, n - pstart), s, id);
+            }
+            dst.id[out] = id;
+            dst.sq[out] = s;
+            dst.aux[out] = ax;
+        }
+        __syncwarp();
+        const Arr tmp = src;
+        src = dst;
+        dst = tmp;
+    }
+    return src;
 }
 
 // ---------------------------------------------------------------------------
@@ -369,19 +401,9 @@ struct TfbReg {
     }
     // W -> R_L (routing.cpp:93 and :242)
     __device__ void flush(Common& c, int lane) {
-        const bool v = static_cast<uint32_t>(lane) < wsize;
-        uint32_t r = 0;
-        for (uint32_t j = 0; j < wsize; ++j) {
-            const float sj = __shfl_sync(FULL, w_sq, j);
-            const uint32_t ij = __shfl_sync(FULL, w_id, j);
-            r += cless(sj, ij, w_sq, w_id) ? 1u : 0u;
-        }
-        if (v) {
-            c.mo.id[r] = w_id;
-            c.mo.sq[r] = w_sq;
-        }
+        rl_append(c, w_id, w_sq, static_cast<uint32_t>(lane) < wsize, lane);
+        c.rl_size += wsize;
         __syncwarp();
-        rl_merge(c, c.mo, wsize, lane);
     }
     // routing.cpp:92-114
     __device__ bool end_round(Common& c, int lane) {
@@ -568,8 +590,9 @@ struct TfbMem {
         recompute_zmax(lane);
     }
     __device__ void flush(Common& c, int lane) {
-        rank_sort(W, c.mo, wsize, lane);
-        rl_merge(c, c.mo, wsize, lane);
+        for (uint32_t i = lane; i < wsize; i += 32) rl_append(c, W.id[i], W.sq[i], true, i);
+        c.rl_size += wsize;
+        __syncwarp();
     }
     __device__ bool end_round(Common& c, int lane) {
         flush(c, lane);
@@ -596,18 +619,18 @@ struct TfbMem {
             zmax_sq = zmax_dist = 0.0f;
             return false;
         }
-        rank_sort(mi, c.mo, nm, lane);
+        const Arr srt = warp_sort(mi, c.mo, nm, lane);
         const uint32_t refill = min(nm, b);
         for (uint32_t i = lane; i < nm; i += 32) {
             if (i < refill) {
-                W.id[i] = c.mo.id[i];
-                W.sq[i] = c.mo.sq[i];
-                W.aux[i] = c.mo.aux[i];
+                W.id[i] = srt.id[i];
+                W.sq[i] = srt.sq[i];
+                W.aux[i] = srt.aux[i];
             } else {
                 const uint32_t p = i - refill;
-                rt.id[p] = c.mo.id[i];
-                rt.sq[p] = c.mo.sq[i];
-                rt.aux[p] = c.mo.aux[i];
+                rt.id[p] = srt.id[i];
+                rt.sq[p] = srt.sq[i];
+                rt.aux[p] = srt.aux[i];
             }
         }
         wsize = refill;
@@ -1042,9 +1065,9 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
     c.stage = reinterpret_cast<float*>(sw + P.off_stage);
     {
         uint8_t* rl = (P.rl_in_smem ? sw : gw) + P.off_rl;
-        const uint32_t cap = P.efS ? P.efS : 1;
-        c.rlA = make_arr(rl, cap);
-        c.rlB = make_arr(rl + 12ull * cap, cap);
+        const uint32_t cap = P.rl_cap;  // >= all W flushes of a query (r_max * b + b)
+        c.rl = make_arr(rl, cap);
+        c.rl_tmp = make_arr(rl + 12ull * cap, cap);
         uint8_t* mg = (P.merge_in_smem ? sw : gw) + P.off_merge;
         c.mo = make_arr(mg + 24ull * P.b, 2 * P.b);
     }
@@ -1070,7 +1093,6 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
             epoch = 1;
         }
         c.epoch = epoch;
-        c.rl_cur = 0;
         c.rl_size = 0;
         c.hs_count = 0;
         c.gt_count = 0;
@@ -1198,8 +1220,12 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
         // final flush (routing.cpp:242) and truncation to K (:244-246)
         PT(2);
         s.flush(c, lane);
-        const uint32_t k_out = min(P.K, c.rl_size);
-        const Arr res = c.rl_cur_arr();
+        // R_L = the min(efS, flushed) smallest, output its first K
+        // (routing.cpp:244-246): the K smallest of all flushed entries
+        const uint32_t k_out = min(P.K, min(c.cap_r, c.rl_size));
+        for (uint32_t i = lane; i < c.rl_size; i += 32) c.rl.aux[i] = 0u;
+        __syncwarp();
+        const Arr res = warp_sort(c.rl, c.rl_tmp, c.rl_size, lane);
         for (uint32_t i = lane; i < k_out; i += 32) {
             P.out_ids[static_cast<uint64_t>(qid) * P.K + i] = res.id[i];
             P.out_sq[static_cast<uint64_t>(qid) * P.K + i] = res.sq[i];
