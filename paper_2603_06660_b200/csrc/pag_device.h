@@ -64,9 +64,8 @@ struct SearchLaunch {
     const uint32_t* qlist;
     // scheduling + scratch
     uint32_t* qcounter;
-    uint64_t* gtab;         // per slot: 1 << gtab_log2 entries
-    uint32_t gtab_log2;
-    uint32_t* slot_epoch;   // per slot
+    uint32_t* gbm;          // per slot: visited bitmap of gbm_words (all zero between queries)
+    uint32_t gbm_words;     // multiple of 4 (>= n / 32)
     uint8_t* gscratch;      // per slot: gscratch_stride bytes
     uint64_t gscratch_stride;
     // layout: per-warp smem and per-slot global regions (byte offsets);

@@ -121,12 +121,6 @@ uint32_t default_L(uint32_t dim) {
     return std::min(std::max(p, lo), hi);
 }
 
-uint32_t ceil_log2(uint64_t x) {
-    uint32_t l = 0;
-    while ((1ull << l) < x) ++l;
-    return l;
-}
-
 // ---------------------------------------------------------------------------
 // Read-only mapping of the index file
 // ---------------------------------------------------------------------------
@@ -172,9 +166,8 @@ struct Replica {
     uint64_t cap_nodes = 0;  // allocated node capacity (refresh grows it)
     size_t bytes = 0;
     // search scratch
-    uint64_t* gtab = nullptr;
-    uint32_t gtab_log2 = 0;
-    uint32_t* slot_epoch = nullptr;
+    uint32_t* gbm = nullptr;  // per-slot visited bitmaps
+    uint32_t gbm_words = 0;
     size_t slots = 0;
     uint8_t* gscratch = nullptr;
     size_t gscratch_bytes = 0;
@@ -255,7 +248,7 @@ void free_replica(Replica& r) {
     cudaSetDevice(r.device);
     for (void* p : {static_cast<void*>(r.rows), static_cast<void*>(r.deg), static_cast<void*>(r.adj),
                     static_cast<void*>(r.refsT), static_cast<void*>(r.entries),
-                    static_cast<void*>(r.gtab), static_cast<void*>(r.slot_epoch),
+                    static_cast<void*>(r.gbm),
                     static_cast<void*>(r.gscratch), static_cast<void*>(r.qcounter),
                     static_cast<void*>(r.d_q), static_cast<void*>(r.d_out), static_cast<void*>(r.bnorm)})
         dev_free(p);
@@ -582,13 +575,9 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     L.warp_smem_bytes = align16(off);
     pl.gscratch_stride = std::max<uint64_t>(256, goff);
     L.gscratch_stride = pl.gscratch_stride;
-    // per-slot HBM visited table
-    uint64_t want = 2ull * (16ull * p.efS + 512ull);
-    L.gtab_log2 = std::max<uint32_t>(std::max<uint32_t>(12, ceil_log2(want)), gt_log2_min);
-    if (const char* e = std::getenv("PAG_GPU_GTAB_LOG2")) {  // test hook: force the overflow path
-        const uint32_t forced = static_cast<uint32_t>(std::atoi(e));
-        if (forced >= 4 && forced < 28) L.gtab_log2 = std::max(forced, gt_log2_min);
-    }
+    // per-slot HBM visited bitmap (n bits, 16-B multiple)
+    L.gbm_words = static_cast<uint32_t>(((ix.n + 127) / 128) * 4);
+    (void)gt_log2_min;
     int bps = 0;
     cuda_check(pagdev::search_occupancy(L, &bps), "occupancy");
     if (bps <= 0) throw_err(PAG_GPU_ERUNTIME, "search configuration does not fit on the GPU");
@@ -600,23 +589,19 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
 void ensure_scratch(Replica& r, Plan& pl) {
     auto& L = pl.L;
     const size_t slots = static_cast<size_t>(pl.grid) * kWarpsPerBlock;
-    if (!std::getenv("PAG_GPU_GTAB_LOG2")) L.gtab_log2 = std::max(L.gtab_log2, r.gtab_log2);  // only grow
-    if (slots > r.slots || L.gtab_log2 != r.gtab_log2) {
+    if (slots > r.slots || L.gbm_words > r.gbm_words) {
         const size_t ns = std::max(slots, r.slots);
-        dev_free(r.gtab);
-        dev_free(r.slot_epoch);
-        r.gtab = nullptr;
-        r.slot_epoch = nullptr;
-        dev_alloc(&r.gtab, (ns << L.gtab_log2) * 8);
-        dev_alloc(&r.slot_epoch, ns * 4);
-        cuda_check(cudaMemset(r.gtab, 0, (ns << L.gtab_log2) * 8), "memset");  // blocking: any stream may follow
-        cuda_check(cudaMemset(r.slot_epoch, 0, ns * 4), "memset");
+        const uint32_t words = std::max(L.gbm_words, r.gbm_words);
+        dev_free(r.gbm);
+        r.gbm = nullptr;
+        dev_alloc(&r.gbm, ns * words * 4ull);
+        cuda_check(cudaMemset(r.gbm, 0, ns * words * 4ull), "memset");  // blocking: any stream may follow
         r.slots = ns;
-        r.gtab_log2 = L.gtab_log2;
+        r.gbm_words = words;
     }
+    L.gbm_words = r.gbm_words;
     grow_dev(reinterpret_cast<void**>(&r.gscratch), &r.gscratch_bytes, r.slots * pl.gscratch_stride);
-    L.gtab = r.gtab;
-    L.slot_epoch = r.slot_epoch;
+    L.gbm = r.gbm;
     L.gscratch = r.gscratch;
     L.qcounter = r.qcounter;
 }
@@ -677,7 +662,7 @@ void search_on_replica(pag_gpu_index& ix, Replica& r, const pag_search_params& p
         cuda_check(cudaMemcpyAsync(d_list, redo.data(), 4 * redo.size(), cudaMemcpyHostToDevice, r.stream),
                    "H2D retry list");
         run_search(ix, r, p, r.d_q, static_cast<uint32_t>(redo.size()), d_list, d_ids, d_sq, d_n, d_st,
-                   r.stream, r.gtab_log2 + grow);
+                   r.stream, grow);
         cuda_check(cudaMemcpyAsync(st.data(), d_st, ob_st, cudaMemcpyDeviceToHost, r.stream), "D2H stats");
         cuda_check(cudaStreamSynchronize(r.stream), "search retry");
     }

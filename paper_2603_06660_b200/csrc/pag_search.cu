@@ -103,14 +103,14 @@ struct Common {
     float* stage;
     float* sqbuf;
     uint32_t* degbuf;
-    // visited marks (routing.hpp:104-105): smem open addressing, spilling to
-    // an epoch-stamped per-slot HBM table once the smem table is half full
+    // visited marks (routing.hpp:104-105): smem open addressing; once the
+    // smem table is half full further marks go to this warp's n-bit HBM
+    // bitmap (one load per lookup, no probe chains), cleared after the query
     uint32_t* hs;
     uint32_t hs_log2, hs_count;
-    uint64_t* gt;
-    uint32_t gt_log2, gt_count, epoch;
+    uint32_t* gbm;
+    uint32_t gbm_words, gt_count;
     bool gt_used, overflow;
-    // R_L double buffer (cap efS) and a scratch array (cap 2b)
     // R_L (routing.hpp:150, capacity efS) is never read during the search:
     // flushed W entries are appended here and the cap-limited sorted list is
     // formed once at the end (the bounded insert keeps the efS smallest, an
@@ -135,14 +135,7 @@ __device__ __forceinline__ bool marked(const Common& c, uint32_t id) {
         h = (h + 1) & mask;
     }
     if (!c.gt_used) return false;
-    const uint32_t gm = (1u << c.gt_log2) - 1;
-    h = hslot(id, c.gt_log2);
-    while (true) {
-        const uint64_t e = c.gt[h];
-        if (static_cast<uint32_t>(e >> 32) != c.epoch) return false;
-        if (static_cast<uint32_t>(e) == id) return true;
-        h = (h + 1) & gm;
-    }
+    return (c.gbm[id >> 5] >> (id & 31u)) & 1u;
 }
 
 // warp-uniform call; lane 0 writes
@@ -156,44 +149,42 @@ __device__ __forceinline__ void mark(Common& c, uint32_t id, int lane) {
         }
         ++c.hs_count;
     } else {
-        const uint32_t cap = 1u << c.gt_log2;
-        if (c.gt_count + 1 >= cap - cap / 4) {
-            c.overflow = true;  // host re-runs this query with a larger table
-            return;
-        }
-        if (lane == 0) {
-            const uint32_t gm = cap - 1;
-            uint32_t h = hslot(id, c.gt_log2);
-            while (static_cast<uint32_t>(c.gt[h] >> 32) == c.epoch) h = (h + 1) & gm;
-            c.gt[h] = (static_cast<uint64_t>(c.epoch) << 32) | id;
-        }
+        if (lane == 0) atomicOr(&c.gbm[id >> 5], 1u << (id & 31u));
         c.gt_used = true;
         ++c.gt_count;
     }
     __syncwarp();
 }
 
-// marks the targets of the lanes in `lanes` (distinct ids). Parallel
-// atomicCAS probing while everything fits the smem half-load budget, else the
-// sequential path (HBM spill, overflow detection).
+// marks the targets of the lanes in `lanes` (distinct ids), in parallel:
+// atomicCAS probing while everything fits the smem half-load budget, else
+// the HBM bitmap.
 __device__ __forceinline__ void mark_many(Common& c, uint32_t lanes, uint32_t w, int lane) {
     const uint32_t np = __popc(lanes);
+    const bool mine = (lanes >> lane) & 1u;
     if (c.hs_count + np <= (1u << c.hs_log2) / 2) {
-        if ((lanes >> lane) & 1u) {
+        if (mine) {
             const uint32_t mask = (1u << c.hs_log2) - 1;
             uint32_t h = hslot(w, c.hs_log2);
             while (atomicCAS(&c.hs[h], EMPTY, w) != EMPTY) h = (h + 1) & mask;
         }
         c.hs_count += np;
-        __syncwarp();
-        return;
+    } else {
+        if (mine) atomicOr(&c.gbm[w >> 5], 1u << (w & 31u));
+        c.gt_used = true;
+        c.gt_count += np;
     }
-    uint32_t rem = lanes;
-    while (rem) {
-        const int j = __ffs(rem) - 1;
-        rem &= rem - 1;
-        mark(c, __shfl_sync(FULL, w, j), lane);
-    }
+    __syncwarp();
+}
+
+// zero this warp's bitmap after a query that used it
+__device__ __forceinline__ void clear_bitmap(Common& c, int lane) {
+    if (!c.gt_used) return;
+    uint4* p = reinterpret_cast<uint4*>(c.gbm);
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+    for (uint32_t i = lane; i < c.gbm_words / 4; i += 32) p[i] = z;
+    c.gt_used = false;
+    __syncwarp();
 }
 
 // number of entries of sorted a[0..n) strictly less than (v, id)
@@ -1074,11 +1065,10 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
     c.cap_r = P.efS;
     c.hs = reinterpret_cast<uint32_t*>(sw + P.off_hash);
     c.hs_log2 = P.hash_log2;
-    c.gt = P.gtab + (static_cast<uint64_t>(slot) << P.gtab_log2);
-    c.gt_log2 = P.gtab_log2;
+    c.gbm = P.gbm + static_cast<uint64_t>(slot) * P.gbm_words;  // zero between queries
+    c.gbm_words = P.gbm_words;
     TFB s;
     s.init(P.b, sw, gw, P);
-    uint32_t epoch = P.slot_epoch[slot];
 
     while (true) {
         uint32_t qi = 0;
@@ -1088,11 +1078,6 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
         const uint32_t qid = P.qlist ? P.qlist[qi] : qi;
 
         // ---- reset (routing.cpp:12-30)
-        if (++epoch == 0) {  // epoch wrap: clear this slot's table
-            for (uint32_t i = lane; i < (1u << c.gt_log2); i += 32) c.gt[i] = 0;
-            epoch = 1;
-        }
-        c.epoch = epoch;
         c.rl_size = 0;
         c.hs_count = 0;
         c.gt_count = 0;
@@ -1241,11 +1226,11 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
             st[kStatEdges] = c.n_edges;
             st[kStatStatus] = c.overflow ? kStatusVisitedOverflow : 0u;
             st[6] = c.hs_count + c.gt_count;  // marks held
-            st[7] = 0;
+            st[7] = c.gt_count;               // of which in the HBM bitmap
         }
+        clear_bitmap(c, lane);
         __syncwarp();
     }
-    if (lane == 0) P.slot_epoch[slot] = epoch;
 #ifdef PAG_PHASE_TIMING
     if (lane == 0)
         for (int k = 0; k < 8; ++k) atomicAdd(&g_phase[k], static_cast<unsigned long long>(c.pt_acc[k]));

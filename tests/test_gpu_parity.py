@@ -76,16 +76,19 @@ def test_search_matches_reference_binary(pag, built, fixture_dir):
     assert_same_results((got.ids, got.sq, got.n_out, got.stats[:, :4]), (ids, sq, n_out, st), "vs reference")
 
 
-def test_visited_overflow_retry_is_exact(pag, built, monkeypatch):
-    """Force a tiny HBM visited table: queries overflow, the host re-runs them
-    with a larger table, results stay bit-identical."""
-    monkeypatch.setenv("PAG_GPU_GTAB_LOG2", "6")
+@pytest.mark.parametrize("hash_log2", ["4", "6"])
+def test_visited_bitmap_spill_is_exact(pag, built, monkeypatch, hash_log2):
+    """Force a tiny smem visited table so nearly every mark spills to the
+    per-warp HBM bitmap (cleared between queries): results stay bit-identical,
+    also across consecutive batches reusing the same bitmaps."""
+    monkeypatch.setenv("PAG_GPU_HASH_LOG2", hash_log2)
     fx = built("deg64")
     ix = pag.load_index(fx["index"])
     try:
-        got = ix.search_batch(fx["queries"], pag.SearchParams(K=10, efS=400))
-        want = O.OracleIndex(fx["index"]).search(fx["queries"], 10, 400)
-        assert_same_results((got.ids, got.sq, got.n_out, got.stats), want, "overflow retry")
+        for K, efS in ((10, 400), (32, 96), (10, 60)):
+            got = ix.search_batch(fx["queries"], pag.SearchParams(K=K, efS=efS))
+            want = O.OracleIndex(fx["index"]).search(fx["queries"], K, efS)
+            assert_same_results((got.ids, got.sq, got.n_out, got.stats), want, f"bitmap spill {K}/{efS}")
     finally:
         ix.close()
 
