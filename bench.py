@@ -460,6 +460,15 @@ def run_pag(args, cfg, paths, rank, world, local_rank, threads, dist):
         if dist is not None:
             dist.destroy_process_group()
         return
+    # ncu DRAM traffic per launch recorded for this workload/mode/efS (profiles/)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            rec = json.load(f).get(args.config)
+        if rec and rec["dist"] == args.dist and rec["efS"] == efs and rec["queries_per_launch"] == nq:
+            traffic = rec["bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        traffic = None
     # cpu baseline (reference search, all host cores, bounded sample)
     cpu = None
     if world == 1 and not args.no_cpu_baseline and os.path.exists(REF_BIN):
@@ -492,8 +501,9 @@ def run_pag(args, cfg, paths, rank, world, local_rank, threads, dist):
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": args.steps,  # one pag_search_kernel launch per step
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind,
-                     "bytes_per_query": round(bytes_total / nq, 1)},
+                     "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
+                     "bytes_per_query": round(bytes_total / nq, 1),
+                     "algorithmic_bytes_per_launch": round(bytes_total, 1)},
         "per_query": {"exact": round(float(sm[:, 0].mean()), 2), "tests": round(float(sm[:, 1].mean()), 2),
                       "passes": round(float(sm[:, 2].mean()), 2), "expansions": round(float(sm[:, 3].mean()), 2),
                       "edges_scanned": round(float(sm[:, 4].mean()), 2)},
