@@ -534,6 +534,7 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     uint32_t off = 0;
     L.off_q = off;
     off = align16(off + 4 * ix.dstride);
+    off = (off + 63u) & ~63u;  // 64-B aligned table (code_sum ORs the code offset into the base)
     L.off_T = off;
     off = align16(off + 4 * ix.L * 16);  // T rows padded to 16 (m <= 16)
     L.off_hash = off;
@@ -572,7 +573,7 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     L.off_rt = L.off_rf + 12 * b;
     place(rl_s, szRL, &L.off_rl, &L.rl_in_smem);
     place(m_s, szM, &L.off_merge, &L.merge_in_smem);
-    L.warp_smem_bytes = align16(off);
+    L.warp_smem_bytes = (off + 63u) & ~63u;  // keeps every warp's table 64-B aligned
     pl.gscratch_stride = std::max<uint64_t>(256, goff);
     L.gscratch_stride = pl.gscratch_stride;
     // per-slot HBM visited bitmap (n bits, 16-B multiple)

@@ -797,15 +797,25 @@ __device__ void dist_fast(const SearchLaunch& P, Common& c, uint32_t items, uint
 #pragma unroll
             for (int r = 0; r < 4; ++r) cur[r] = nxt[r];
         }
+        // transpose-reduce the 4 row partials in 6 shuffles: after the xor-16
+        // and xor-8 exchanges lane group 8r..8r+7 holds row r, then a 3-step tree
+        const bool h16 = lane & 16, h8 = lane & 8;
+        const float p0 = part[0].x + part[0].y, p1 = part[1].x + part[1].y;
+        const float p2 = part[2].x + part[2].y, p3 = part[3].x + part[3].y;
+        float k0 = h16 ? p2 : p0, k1 = h16 ? p3 : p1;
+        k0 += __shfl_xor_sync(FULL, h16 ? p0 : p2, 16);
+        k1 += __shfl_xor_sync(FULL, h16 ? p1 : p3, 16);
+        float v = h8 ? k1 : k0;
+        v += __shfl_xor_sync(FULL, h8 ? k0 : k1, 8);
+        v += __shfl_xor_sync(FULL, v, 4);
+        v += __shfl_xor_sync(FULL, v, 2);
+        v += __shfl_xor_sync(FULL, v, 1);
+        const int row = lane >> 3;
+        int jrow = jr[0];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            if (r < nb) {
-                float v = part[r].x + part[r].y;
-#pragma unroll
-                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-                if (lane == 0) c.sqbuf[jr[r]] = v;
-            }
-        }
+        for (int r = 1; r < 4; ++r)
+            if (r == row) jrow = jr[r];
+        if ((lane & 7) == 0 && row < nb) c.sqbuf[jrow] = v;
     }
 }
 
@@ -844,11 +854,31 @@ __device__ float query_norm(const float* q, uint32_t D, int lane) {
 // table sum of one edge's codes (projection.cpp:145-149), serial in l.
 // T is stored with a row stride of 16 (m <= 16), so l*16 + code needs no
 // multiply; fully unrolled for the default subspace counts.
+template <int L0, int LL>
+struct CodeSumStep {  // subspace L0 of LL, compile-time unrolled (immediate row offset)
+    __device__ __forceinline__ static void run(float& sum, uint32_t tb, const uint32_t (&cw)[4]) {
+        const uint32_t w = cw[L0 >> 3];
+        constexpr int sh = 4 * (L0 & 7) - 2;
+        const uint32_t off = ((sh >= 0) ? (w >> (sh >= 0 ? sh : 0)) : (w << 2)) & 0x3Cu;
+        float v;
+        asm("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(off | tb), "n"(L0 * 64));
+        sum = __fadd_rn(sum, v);
+        CodeSumStep<L0 + 1, LL>::run(sum, tb, cw);
+    }
+};
+template <int LL>
+struct CodeSumStep<LL, LL> {
+    __device__ __forceinline__ static void run(float&, uint32_t, const uint32_t (&)[4]) {}
+};
+
 template <int LL>
 __device__ __forceinline__ float code_sum_fixed(const float* T, const uint32_t (&cw)[4]) {
+    // T is 64-B aligned in smem, so (4 * code) | base is the entry of row 0 and
+    // the row offset l * 64 folds into the load's immediate: shift, and-or,
+    // load, add per subspace
+    const uint32_t tb = static_cast<uint32_t>(__cvta_generic_to_shared(T));
     float sum = 0.0f;
-#pragma unroll
-    for (int l = 0; l < LL; ++l) sum = __fadd_rn(sum, T[l * 16 + ((cw[l >> 3] >> (4 * (l & 7))) & 15u)]);
+    CodeSumStep<0, LL>::run(sum, tb, cw);
     return sum;
 }
 
@@ -954,6 +984,7 @@ __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
         const unsigned long long key =
             cand ? static_cast<unsigned long long>(w) : ((1ull << 32) | static_cast<unsigned>(lane));
         const uint32_t same = __match_any_sync(FULL, key) & cand_mask;
+        const bool any_dup = __any_sync(FULL, __popc(same) > 1);
 
         // (i) speculative PRT at the group-start radius
         const float adist0 = s.admission_dist();
@@ -985,8 +1016,10 @@ __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
         while (rem) {
             const int jl = __ffs(rem) - 1;
             rem &= rem - 1;
-            const uint32_t same_j = __shfl_sync(FULL, same, jl);
-            if (same_j & ((1u << jl) - 1u) & passed) continue;  // marked earlier in this group
+            if (any_dup) {  // rare: a target repeated inside this group
+                const uint32_t same_j = __shfl_sync(FULL, same, jl);
+                if (same_j & ((1u << jl) - 1u) & passed) continue;  // marked earlier in this group
+            }
             const float en_j = __shfl_sync(FULL, en, jl);
             const float quot_j = __shfl_sync(FULL, quot, jl);
             const float tau0_j = __shfl_sync(FULL, tau0, jl);
@@ -1036,7 +1069,7 @@ template <class TFB, bool EXACT, int NCH>
 #define PAG_MIN_BLOCKS 4
 #endif
 __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const __grid_constant__ SearchLaunch P) {
-    extern __shared__ __align__(16) uint8_t smem[];
+    extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const uint32_t slot = blockIdx.x * P.warps_per_block + wib;
