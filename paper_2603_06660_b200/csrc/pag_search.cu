@@ -751,6 +751,51 @@ __device__ void dist_exact(const SearchLaunch& P, Common& c, uint32_t items, uin
     }
 }
 
+// Warp-tree distances, two rows at a time: each half-warp owns one row and
+// every lane issues all of its 2*NCH float4 loads back to back (one memory
+// latency per row pair instead of one per 128-float chunk), then a 16-lane
+// xor tree. For NCH <= 6 (padded_dim <= 768).
+template <int NCH>
+__device__ void dist_fast_pairs(const SearchLaunch& P, Common& c, uint32_t items, uint32_t w, int lane) {
+    constexpr int NL = 2 * NCH;  // float4 loads per lane per row
+    const IndexView& ix = P.ix;
+    const uint32_t DS = 128u * NCH;
+    const int half = lane >> 4, hl = lane & 15;
+    uint32_t rest = items;
+    while (rest) {
+        const int j0 = __ffs(rest) - 1;
+        rest &= rest - 1;
+        int j1 = j0;
+        bool two = false;
+        if (rest) {
+            j1 = __ffs(rest) - 1;
+            rest &= rest - 1;
+            two = true;
+        }
+        const int jm = half ? j1 : j0;
+        const uint32_t wr = __shfl_sync(FULL, w, jm);
+        const float* rp = ix.rows + static_cast<uint64_t>(wr) * DS + 4u * hl;
+        float4 v[NL];
+#pragma unroll
+        for (int i = 0; i < NL; ++i) v[i] = ldg_f4(rp + 64 * i);
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < NL; ++i) {
+            const float4 qv = *reinterpret_cast<const float4*>(c.q + 64 * i + 4 * hl);
+            const float2 dlo = __fadd2_rn(make_float2(v[i].x, v[i].y), make_float2(-qv.x, -qv.y));
+            const float2 dhi = __fadd2_rn(make_float2(v[i].z, v[i].w), make_float2(-qv.z, -qv.w));
+            acc = __ffma2_rn(dlo, dlo, acc);
+            acc = __ffma2_rn(dhi, dhi, acc);
+        }
+        float s = acc.x + acc.y;
+        s += __shfl_xor_sync(FULL, s, 8);
+        s += __shfl_xor_sync(FULL, s, 4);
+        s += __shfl_xor_sync(FULL, s, 2);
+        s += __shfl_xor_sync(FULL, s, 1);
+        if (hl == 0 && (half == 0 || two)) c.sqbuf[jm] = s;
+    }
+}
+
 template <int NCH>
 __device__ void dist_fast(const SearchLaunch& P, Common& c, uint32_t items, uint32_t w, int lane) {
     const IndexView& ix = P.ix;
@@ -832,7 +877,13 @@ __device__ __forceinline__ void distances(const SearchLaunch& P, Common& c, uint
     if (EXACT)
         dist_exact<NCH>(P, c, items, w, lane);
     else
-        dist_fast<NCH>(P, c, items, w, lane);
+    {
+        if constexpr (NCH > 0 && NCH <= 6) {
+            dist_fast_pairs<NCH>(P, c, items, w, lane);
+        } else {
+            dist_fast<NCH>(P, c, items, w, lane);
+        }
+    }
     if (mine) c.degbuf[lane] = deg;
     __syncwarp();
 }
