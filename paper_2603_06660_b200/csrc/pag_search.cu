@@ -878,7 +878,7 @@ __device__ __forceinline__ void distances(const SearchLaunch& P, Common& c, uint
         dist_exact<NCH>(P, c, items, w, lane);
     else
     {
-        if constexpr (NCH > 0 && NCH <= 6) {
+        if constexpr (NCH > 0 && NCH <= 8) {
             dist_fast_pairs<NCH>(P, c, items, w, lane);
         } else {
             dist_fast<NCH>(P, c, items, w, lane);
