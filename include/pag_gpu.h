@@ -48,7 +48,7 @@ typedef struct pag_search_stats {
 } pag_search_stats;
 
 /* Search knobs: proj/include/pag/routing.hpp:13-22 (SearchParams).
- * collect_pes is build-only and not part of the query path. */
+ * collect_pes (build-only) is an argument of pag_gpu_construction_search. */
 typedef struct pag_search_params {
     uint32_t K;          /* default 10 */
     uint32_t efS;        /* default 100 */
@@ -76,7 +76,9 @@ int pag_gpu_open(const char* index_path, uint32_t device_mask, pag_gpu_index** o
 int pag_gpu_close(pag_gpu_index* ix);
 
 /* info[0..11] = n, dim, padded_dim, L, m, M, metric (0 euclidean, 1 cosine),
- * n_entries, seed, total_edges, n_devices, device_bytes_per_replica.
+ * n_entries, seed, total_edges, n_devices, device_bytes_per_replica;
+ * info[12] = tensor-core ground-truth queries re-run exactly so far;
+ * info[13..15] = the header's efC, b_build, enable_pes.
  * Replaces the PagIndex/VectorSet accessors (builder.hpp:71-91). */
 int pag_gpu_info(const pag_gpu_index* ix, uint64_t* info, size_t n_info);
 
@@ -102,6 +104,25 @@ int pag_gpu_search(pag_gpu_index* ix, const float* q, uint64_t nq,
 int pag_gpu_search_device(pag_gpu_index* ix, const float* q_dev, uint64_t nq,
                           const pag_search_params* params, uint32_t* ids_dev, float* sq_dev,
                           uint32_t* n_out_dev, uint32_t* stats_dev, void* stream);
+
+/* Construction search. Replaces the search step of
+ *   insert_with_state(PagIndex&, uint32_t v, PesSet&, TfbState&)
+ *   proj/src/builder.cpp:218-227 — search_padded(index, vectors().row(v), sp)
+ *   with sp.K = sp.efS = efC, sp.b_override = b_build, sp.collect_pes =
+ *   enable_pes (proj/include/pag/routing.hpp:186-187, proj/src/routing.cpp:206-247)
+ * — batched over nodes already in the resident index: the query of node
+ * nodes[i] is its stored row (no padding or normalisation). params NULL =
+ * the header's efC / b_build; collect_pes < 0 = the header's enable_pes.
+ * SearchResult.pes_rejected (routing.hpp:176, routing.cpp:190-199,235): up
+ * to pes_cap expanded ids per node in pes[i * pes_cap ...], in expansion
+ * order; pes_n[i] = the full count (> pes_cap means truncated). Results are
+ * bit-identical to the reference (reference-order distances) unless
+ * params->exact_dist = 0. Errors: "node id out of range" (EINVAL), plus
+ * those of pag_gpu_search. */
+int pag_gpu_construction_search(pag_gpu_index* ix, const uint32_t* nodes, uint64_t nn,
+                                const pag_search_params* params, int collect_pes, uint32_t* ids, float* sq,
+                                uint32_t* n_out, pag_search_stats* stats, uint32_t* pes, uint32_t pes_cap,
+                                uint32_t* pes_n);
 
 /* Replaces: GroundTruth ground_truth(const VectorSet& base,
  *                                    const VectorSet& queries, uint32_t k_star)

@@ -71,6 +71,9 @@ def lib():
         "pago_search": (C.c_int, [P, f32p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                   C.c_int, C.c_int, u32p, f32p, u32p, u64p]),
         "pago_query_table": (C.c_int, [P, f32p, f32p]),
+        "pago_construction_search": (C.c_int, [P, u32p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                               C.c_int, u32p, f32p, u32p, u64p, u32p, C.c_uint32, u32p]),
+        "pago_build_params": (None, [P, u32p]),
         "pago_ground_truth": (C.c_int, [f32p, C.c_uint64, f32p, C.c_uint64, C.c_uint32,
                                         C.c_uint32, u32p, f32p]),
         "pago_recall_at_k": (C.c_double, [u32p, C.c_size_t, u32p, f32p, C.c_size_t, C.c_uint32]),
@@ -119,6 +122,9 @@ class OracleIndex:
         (self.n, self.dim, self.padded, self.L, self.m, self.M, self.metric,
          self.n_entries, self.seed, self.total_edges) = (int(x) for x in info)
         self.sub_dim = self.padded // self.L
+        bp = np.zeros(4, np.uint32)
+        lib().pago_build_params(self._h, bp)
+        self.efC, self.b_build, self.enable_pes, self.pes_flush = (int(x) for x in bp)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -165,6 +171,27 @@ class OracleIndex:
                                  K, efS, b_override, int(use_prt), int(use_tfb),
                                  ids.reshape(-1), sq.reshape(-1), n_out, stats.reshape(-1)))
         return ids, sq, n_out, stats
+
+    def construction_search(self, nodes, K=None, efS=None, b_override=None, collect_pes=None,
+                            pes_cap: int = 256):
+        """insert_with_state's search (builder.cpp:218-227) for existing nodes:
+        returns (ids, sq, n_out, stats[nn,5], pes[nn,pes_cap], pes_n)."""
+        nodes = np.ascontiguousarray(nodes, np.uint32).reshape(-1)
+        K = self.efC if K is None else K
+        efS = self.efC if efS is None else efS
+        b = self.b_build if b_override is None else b_override
+        pes_on = bool(self.enable_pes) if collect_pes is None else bool(collect_pes)
+        nn = len(nodes)
+        ids = np.full((nn, max(K, 1)), 0xFFFFFFFF, np.uint32)
+        sq = np.zeros((nn, max(K, 1)), np.float32)
+        n_out = np.zeros(nn, np.uint32)
+        stats = np.zeros((nn, 5), np.uint64)
+        pes = np.zeros((nn, max(pes_cap, 1)), np.uint32)
+        pes_n = np.zeros(nn, np.uint32)
+        _check(lib().pago_construction_search(self._h, nodes if nn else np.zeros(1, np.uint32), nn, K, efS, b,
+                                              int(pes_on), ids.reshape(-1), sq.reshape(-1), n_out,
+                                              stats.reshape(-1), pes.reshape(-1), pes_cap, pes_n))
+        return ids[:, :K], sq[:, :K], n_out, stats, pes[:, :pes_cap], pes_n
 
     def query_table(self, q: np.ndarray) -> np.ndarray:
         out = np.zeros(self.L * self.m, np.float32)
@@ -226,6 +253,22 @@ def ref_search(index: str, queries: str, K: int, efS: int, out: str, **kw):
         n_out = np.frombuffer(f.read(nq * 4), np.uint32)
         stats = np.frombuffer(f.read(nq * 32), np.uint64).reshape(nq, 4)
     return ids, sq, n_out, stats, timing
+
+
+def ref_build_search(index: str, count: int, stride: int, out: str, **kw):
+    """The reference's construction search (search_padded with collect_pes) for
+    nodes (i * stride) % n; returns (nodes, ids, sq, n_out, stats[nn,4], pes, pes_n, timing)."""
+    txt = ref_run("build-search", index=index, count=count, stride=stride, out=out, **kw)
+    timing = json.loads(txt.strip().splitlines()[-1])
+    with open(out, "rb") as f:
+        nn, k, cap = (int(x) for x in np.frombuffer(f.read(24), np.uint64))
+        ids = np.frombuffer(f.read(nn * k * 4), np.uint32).reshape(nn, k)
+        sq = np.frombuffer(f.read(nn * k * 4), np.float32).reshape(nn, k)
+        n_out = np.frombuffer(f.read(nn * 4), np.uint32)
+        stats = np.frombuffer(f.read(nn * 32), np.uint64).reshape(nn, 4)
+        pes_n = np.frombuffer(f.read(nn * 4), np.uint32)
+        pes = np.frombuffer(f.read(nn * cap * 4), np.uint32).reshape(nn, cap)
+    return ids, sq, n_out, stats, pes, pes_n, timing
 
 
 def ref_gt(base: str, queries: str, k: int, out: str, threads: int = 1):

@@ -661,15 +661,19 @@ typedef struct {
     uint64_t exact, test, pass, visited, edges;
 } stats5;
 
-/* routing.cpp:139-204 (the PES tracking lines 190-199 are build-only) */
-static void expand_node(size_t work_idx, struct pago_tfb* st, const pago_index* ix, const float* q,
-                        int use_prt, stats5* stats) {
+/* routing.cpp:139-204. With collect_pes (the construction search,
+   builder.cpp:218-224) the PES margin of every edge is tracked
+   (routing.cpp:150,190-199) and the return value is out.pes_rejected. */
+static int expand_node(size_t work_idx, struct pago_tfb* st, const pago_index* ix, const float* q,
+                       int use_prt, int collect_pes, stats5* stats) {
     went* entry = &st->W[work_idx];
     entry->visited = 1;
     ++stats->visited;
     const uint32_t u = entry->id;
     const float dist_uq = sqrtf(entry->sq);
     const int exact_mode = (dist_uq == 0.0f) || !use_prt;
+    const int track_pes = collect_pes && dist_uq > 0.0f;
+    float pes_max = -INFINITY;
     const uint32_t deg = ix->degree[u];
     const uint32_t* tg = ix->targets + (size_t)u * ix->maxdeg;
     const float* sc = ix->scalars + (size_t)u * ix->maxdeg * 3;
@@ -677,43 +681,59 @@ static void expand_node(size_t work_idx, struct pago_tfb* st, const pago_index* 
     for (uint32_t j = 0; j < deg; ++j) {
         const uint32_t w = tg[j];
         const float cos_beta = sc[3 * j + 0], edge_norm = sc[3 * j + 1], base_off = sc[3 * j + 2];
-        if (tfb_marked(st, w)) continue;
-        ++stats->test;
-        int pass;
-        if (exact_mode) {
-            pass = 1;
-        } else {
-            float tau = pago_prt_threshold(edge_norm, dist_uq, tfb_admission_dist(st));
-            if (tau >= 1.0f + 1e-6f) {
-                pass = 0;
-            } else if (tau <= -1.0f) {
+        const uint8_t* codes = ix->codes + ((size_t)u * ix->maxdeg + j) * ix->cb;
+        float quot = 0.0f;
+        int have_quot = 0;
+        if (!tfb_marked(st, w)) {
+            ++stats->test;
+            int pass;
+            if (exact_mode) {
                 pass = 1;
             } else {
-                const uint8_t* codes = ix->codes + ((size_t)u * ix->maxdeg + j) * ix->cb;
-                /* projection.hpp:71-74 */
-                float quot = ((pago_table_code_sum(st->table, ix->L, ix->m, codes) - base_off) /
-                              dist_uq) /
-                             cos_beta;
-                pass = quot >= tau;
+                float tau = pago_prt_threshold(edge_norm, dist_uq, tfb_admission_dist(st));
+                if (tau >= 1.0f + 1e-6f) {
+                    pass = 0;
+                } else if (tau <= -1.0f) {
+                    pass = 1;
+                } else {
+                    /* projection.hpp:71-74 */
+                    quot = ((pago_table_code_sum(st->table, ix->L, ix->m, codes) - base_off) /
+                            dist_uq) /
+                           cos_beta;
+                    have_quot = 1;
+                    pass = quot >= tau;
+                }
+            }
+            if (pass) {
+                ++stats->pass;
+                float sq = pago_sq_dist(ix->rows + (size_t)w * ix->padded, q, ix->padded);
+                ++stats->exact;
+                tfb_mark(st, w);
+                if (sq < tfb_admission_sq(st))
+                    tfb_admit(st, w, sq);
+                else
+                    ring_push(&st->rf, (cand){w, sq});
             }
         }
-        if (pass) {
-            ++stats->pass;
-            float sq = pago_sq_dist(ix->rows + (size_t)w * ix->padded, q, ix->padded);
-            ++stats->exact;
-            tfb_mark(st, w);
-            if (sq < tfb_admission_sq(st))
-                tfb_admit(st, w, sq);
-            else
-                ring_push(&st->rf, (cand){w, sq});
+        if (track_pes) { /* routing.cpp:190-199, std::max(pes_max, quot - delta) */
+            if (!have_quot)
+                quot = ((pago_table_code_sum(st->table, ix->L, ix->m, codes) - base_off) /
+                        dist_uq) /
+                       cos_beta;
+            const float delta = edge_norm / (2.0f * dist_uq);
+            const float x = quot - delta;
+            if (pes_max < x) pes_max = x;
         }
     }
+    return track_pes && pes_max < 0.0f;
 }
 
 /* routing.cpp:206-247 */
 static int search_padded(const pago_index* ix, const float* q, uint32_t K, uint32_t efS,
-                         uint32_t b_override, int use_prt, int use_tfb, struct pago_tfb* st,
-                         uint32_t* ids, float* sq, uint32_t* n_out, stats5* stats) {
+                         uint32_t b_override, int use_prt, int use_tfb, int collect_pes,
+                         struct pago_tfb* st, uint32_t* ids, float* sq, uint32_t* n_out,
+                         stats5* stats, uint32_t* pes, uint32_t pes_cap, uint32_t* pes_n) {
+    uint32_t npes = 0;
     const uint32_t n = (uint32_t)ix->n;
     const uint32_t bdef = b_override ? b_override : (K > 10u ? K : 10u);
     const uint32_t b = use_tfb ? bdef : (efS > bdef ? efS : bdef);
@@ -732,7 +752,13 @@ static int search_padded(const pago_index* ix, const float* q, uint32_t K, uint3
     }
     for (uint32_t r = 0; r < r_max; ++r) {
         int64_t i;
-        while ((i = tfb_next_unvisited(st)) >= 0) expand_node((size_t)i, st, ix, q, use_prt, stats);
+        while ((i = tfb_next_unvisited(st)) >= 0) {
+            const uint32_t u = st->W[i].id;
+            if (expand_node((size_t)i, st, ix, q, use_prt, collect_pes, stats)) { /* :235 */
+                if (npes < pes_cap) pes[npes] = u;
+                ++npes;
+            }
+        }
         if (r + 1 == r_max || !tfb_end_round(st)) break;
     }
     for (size_t i = 0; i < st->wsize; ++i) tfb_push_result(st, (cand){st->W[i].id, st->W[i].sq});
@@ -742,6 +768,7 @@ static int search_padded(const pago_index* ix, const float* q, uint32_t K, uint3
         sq[i] = st->R[i].sq;
     }
     *n_out = (uint32_t)k;
+    if (pes_n) *pes_n = npes;
     return PAGO_OK;
 }
 
@@ -771,8 +798,8 @@ int pago_search(const pago_index* ix, const float* q, uint64_t nq, uint32_t K, u
         rc = prep_query(ix, q + i * ix->dim, qbuf);
         if (rc) break;
         stats5 s = {0, 0, 0, 0, 0};
-        search_padded(ix, qbuf, K, efS, b_override, use_prt, use_tfb, &st, ids + i * K,
-                      sq + i * K, n_out + i, &s);
+        search_padded(ix, qbuf, K, efS, b_override, use_prt, use_tfb, 0, &st, ids + i * K,
+                      sq + i * K, n_out + i, &s, NULL, 0, NULL);
         if (stats) {
             stats[i * 5 + 0] = s.exact;
             stats[i * 5 + 1] = s.test;
@@ -790,6 +817,51 @@ int pago_search(const pago_index* ix, const float* q, uint64_t nq, uint32_t K, u
     free(st.merge);
     free(st.marks);
     return rc;
+}
+
+/* insert_with_state's search (builder.cpp:218-227): the query is the node's
+   own stored (padded, already normalised) row, passed to search_padded
+   directly; SearchResult.pes_rejected (routing.hpp:176) per node, at most
+   pes_cap ids kept, pes_n = the full count. */
+int pago_construction_search(const pago_index* ix, const uint32_t* nodes, uint64_t nn, uint32_t K,
+                             uint32_t efS, uint32_t b_override, int collect_pes, uint32_t* ids,
+                             float* sq, uint32_t* n_out, uint64_t* stats, uint32_t* pes,
+                             uint32_t pes_cap, uint32_t* pes_n) {
+    if (ix->n == 0) return fail(PAGO_ERUNTIME, "search on empty index");
+    if (K > efS) return fail(PAGO_EINVAL, "K > efS");
+    for (uint64_t i = 0; i < nn; ++i)
+        if (nodes[i] >= ix->n) return fail(PAGO_EINVAL, "node id out of range");
+    struct pago_tfb st;
+    memset(&st, 0, sizeof st);
+    st.table = (float*)malloc(sizeof(float) * (size_t)ix->L * (ix->m ? ix->m : 1));
+    for (uint64_t i = 0; i < nn; ++i) {
+        stats5 s = {0, 0, 0, 0, 0};
+        search_padded(ix, ix->rows + (size_t)nodes[i] * ix->padded, K, efS, b_override, 1, 1,
+                      collect_pes, &st, ids + i * K, sq + i * K, n_out + i, &s,
+                      pes + i * pes_cap, pes_cap, pes_n + i);
+        if (stats) {
+            stats[i * 5 + 0] = s.exact;
+            stats[i * 5 + 1] = s.test;
+            stats[i * 5 + 2] = s.pass;
+            stats[i * 5 + 3] = s.visited;
+            stats[i * 5 + 4] = s.edges;
+        }
+    }
+    free(st.table);
+    free(st.W);
+    free(st.rf.buf);
+    free(st.rt.buf);
+    free(st.R);
+    free(st.merge);
+    free(st.marks);
+    return PAGO_OK;
+}
+
+void pago_build_params(const pago_index* ix, uint32_t* out) {
+    out[0] = ix->efC;
+    out[1] = ix->b_build;
+    out[2] = ix->enable_pes;
+    out[3] = ix->pes_flush;
 }
 
 int pago_query_table(const pago_index* ix, const float* q, float* out) {

@@ -81,6 +81,17 @@ const float* pago_row(const pago_index* ix, uint32_t i);
 int pago_search(const pago_index* ix, const float* q, uint64_t nq, uint32_t K, uint32_t efS,
                 uint32_t b_override, int use_prt, int use_tfb, uint32_t* ids, float* sq,
                 uint32_t* n_out, uint64_t* stats);
+/* Construction search (builder.cpp:218-227 insert_with_state): query = the
+ * stored row of nodes[i]; PES margins tracked when collect_pes
+ * (routing.cpp:150,190-199). pes: nn x pes_cap expanded node ids whose PES
+ * max was negative, in expansion order (routing.cpp:235); pes_n: full count
+ * per node (entries beyond pes_cap are counted, not stored). */
+int pago_construction_search(const pago_index* ix, const uint32_t* nodes, uint64_t nn, uint32_t K,
+                             uint32_t efS, uint32_t b_override, int collect_pes, uint32_t* ids,
+                             float* sq, uint32_t* n_out, uint64_t* stats, uint32_t* pes,
+                             uint32_t pes_cap, uint32_t* pes_n);
+/* out[0..3] = efC, b_build, enable_pes, pes_flush_interval from the header */
+void pago_build_params(const pago_index* ix, uint32_t* out);
 /* projection table of one raw query (after the same pad/normalise as search) */
 int pago_query_table(const pago_index* ix, const float* q, float* out);
 

@@ -211,6 +211,79 @@ int cmd_search(const Args& a) {
     return 0;
 }
 
+// insert_with_state's search (builder.cpp:218-227) over a saved index: the
+// query of node v is its stored padded row, K = efS = efC, b = b_build,
+// collect_pes = enable_pes (each overridable). Nodes are (i * stride) % n.
+int cmd_build_search(const Args& a) {
+    PagIndex index = load_index(a.get("index"));
+    const BuildParams& bp = index.params();
+    const size_t n = index.size();
+    const size_t count = std::stoull(a.get("count", "100"));
+    const size_t stride = std::stoull(a.get("stride", "1"));
+    SearchParams sp;
+    sp.K = std::stoul(a.get("K", std::to_string(bp.efC)));
+    sp.efS = std::stoul(a.get("efS", std::to_string(bp.efC)));
+    sp.b_override = std::stoul(a.get("b", std::to_string(bp.b_build)));
+    sp.collect_pes = a.has("pes") ? a.get("pes") == "1" : bp.enable_pes;
+    const uint32_t pes_cap = std::stoul(a.get("pes-cap", "256"));
+    unsigned threads = static_cast<unsigned>(std::stoul(a.get("threads", "1")));
+    int reps = std::stoi(a.get("reps", "1"));
+    const uint32_t K = sp.K;
+    std::vector<uint32_t> nodes(count);
+    for (size_t i = 0; i < count; ++i) nodes[i] = static_cast<uint32_t>((i * stride) % n);
+    std::vector<uint32_t> ids(count * K, 0xFFFFFFFFu), nout(count, 0), pes(count * pes_cap, 0), pes_n(count, 0);
+    std::vector<float> sq(count * K, 0.0f);
+    std::vector<uint64_t> st(count * 4, 0);
+    auto run_one = [&](size_t i, TfbState& state) {
+        SearchResult r = search_padded(index, index.vectors().row(nodes[i]), sp, state);
+        nout[i] = static_cast<uint32_t>(r.results.size());
+        for (size_t j = 0; j < r.results.size(); ++j) {
+            ids[i * K + j] = r.results[j].id;
+            sq[i * K + j] = r.results[j].sq;
+        }
+        st[i * 4 + 0] = r.stats.exact_dist_count;
+        st[i * 4 + 1] = r.stats.test_count;
+        st[i * 4 + 2] = r.stats.pass_count;
+        st[i * 4 + 3] = r.stats.visited_count;
+        pes_n[i] = static_cast<uint32_t>(r.pes_rejected.size());
+        for (size_t j = 0; j < r.pes_rejected.size() && j < pes_cap; ++j) pes[i * pes_cap + j] = r.pes_rejected[j];
+    };
+    auto sweep = [&]() {
+        std::atomic<size_t> next{0};
+        std::vector<std::thread> pool;
+        for (unsigned t = 0; t < std::max(1u, threads); ++t)
+            pool.emplace_back([&] {
+                TfbState state;
+                size_t i;
+                while ((i = next.fetch_add(1)) < count) run_one(i, state);
+            });
+        for (auto& th : pool) th.join();
+    };
+    if (!a.has("no-warm")) sweep();
+    double total = 0;
+    for (int r = 0; r < reps; ++r) {
+        auto t0 = clk::now();
+        sweep();
+        total += std::chrono::duration<double>(clk::now() - t0).count();
+    }
+    if (a.has("out")) {
+        std::FILE* f = std::fopen(a.get("out").c_str(), "wb");
+        if (!f) throw std::runtime_error("cannot open output");
+        uint64_t hdr[3] = {count, K, pes_cap};
+        write_all(f, hdr, sizeof hdr);
+        write_all(f, ids.data(), ids.size() * 4);
+        write_all(f, sq.data(), sq.size() * 4);
+        write_all(f, nout.data(), nout.size() * 4);
+        write_all(f, st.data(), st.size() * 8);
+        write_all(f, pes_n.data(), pes_n.size() * 4);
+        write_all(f, pes.data(), pes.size() * 4);
+        std::fclose(f);
+    }
+    std::printf("{\"nodes\": %zu, \"threads\": %u, \"reps\": %d, \"seconds_mean\": %.6f, \"qps\": %.3f}\n",
+                count, threads, reps, total / std::max(1, reps), reps ? count / (total / reps) : 0.0);
+    return 0;
+}
+
 int cmd_gt(const Args& a) {
     MetricKind metric = metric_of(a.get("metric", "euclidean"));
     VectorSet base = load_vectors(a.get("base"), VecFormat::fvecs, metric);
@@ -325,7 +398,7 @@ int cmd_sqdist(const Args& a) {
 int main(int argc, char** argv) {
     if (argc < 2) {
         std::fprintf(stderr,
-                     "usage: pag_ref {gen-synthetic|build|search|gt|refs|tables|sqdist|insert} "
+                     "usage: pag_ref {gen-synthetic|build|search|build-search|gt|refs|tables|sqdist|insert} "
                      "--key=value ...\n");
         return 2;
     }
@@ -340,6 +413,7 @@ int main(int argc, char** argv) {
         if (cmd == "tables") return cmd_tables(a);
         if (cmd == "sqdist") return cmd_sqdist(a);
         if (cmd == "insert") return cmd_insert(a);
+        if (cmd == "build-search") return cmd_build_search(a);
     } catch (const std::exception& e) {
         std::fprintf(stderr, "error: %s\n", e.what());
         return 1;

@@ -62,6 +62,14 @@ struct SearchLaunch {
     uint32_t* out_stats;  // nq x kStatWords
     // optional subset of query indices to run (retry path); null = all
     const uint32_t* qlist;
+    // construction search (builder.cpp:218-227): query i is the stored row of
+    // node qnodes[i] (queries unused); with collect_pes the expanded nodes
+    // whose PES max is negative (routing.cpp:190-199,235) go to
+    // out_pes[i * pes_cap ...], the full count to out_pes_n[i]
+    const uint32_t* qnodes;
+    uint32_t collect_pes, pes_cap;
+    uint32_t* out_pes;
+    uint32_t* out_pes_n;
     // scheduling + scratch
     uint32_t* qcounter;
     uint32_t* gbm;          // per slot: visited bitmap of gbm_words (all zero between queries)

@@ -612,17 +612,33 @@ void validate_params(const pag_gpu_index& ix, const pag_search_params& p) {
     if (p.K > p.efS) throw_err(PAG_GPU_EINVAL, "K > efS");                // routing.cpp:209
 }
 
+// construction search (builder.cpp:218-227) device-side extras
+struct ConstructionArgs {
+    const uint32_t* nodes = nullptr;  // device: query i = stored row of nodes[i]
+    uint32_t collect_pes = 0, pes_cap = 0;
+    uint32_t* pes = nullptr;          // device: nq x pes_cap
+    uint32_t* pes_n = nullptr;        // device: nq
+};
+
 // Runs nq queries already on the replica's device. Device buffers:
 // q (nq x dim), ids/sq (nq x K), n_out (nq), stats (nq x 8). qlist optional.
 void run_search(pag_gpu_index& ix, Replica& r, const pag_search_params& p, const float* q_dev,
                 uint32_t nq, const uint32_t* qlist, uint32_t* ids, float* sq, uint32_t* n_out,
-                uint32_t* stats, cudaStream_t stream, uint32_t gt_log2_min) {
+                uint32_t* stats, cudaStream_t stream, uint32_t gt_log2_min,
+                const ConstructionArgs* ca = nullptr) {
     if (nq == 0) return;
     Plan pl = make_plan(ix, r, p, nq, gt_log2_min);
     ensure_scratch(r, pl);
     auto& L = pl.L;
     L.queries = q_dev;
     L.qlist = qlist;
+    if (ca) {
+        L.qnodes = ca->nodes;
+        L.collect_pes = ca->collect_pes;
+        L.pes_cap = ca->pes_cap;
+        L.out_pes = ca->pes;
+        L.out_pes_n = ca->pes_n;
+    }
     L.out_ids = ids;
     L.out_sq = sq;
     L.out_n = n_out;
@@ -631,24 +647,45 @@ void run_search(pag_gpu_index& ix, Replica& r, const pag_search_params& p, const
     cuda_check(pagdev::launch_search(L, pl.grid, stream), "search kernel launch");
 }
 
+// host-side construction request: nodes (host ids) and PES outputs
+struct ConstructionHost {
+    const uint32_t* nodes;
+    uint32_t collect_pes, pes_cap;
+    uint32_t* pes;    // nq x pes_cap (may be null when pes_cap == 0)
+    uint32_t* pes_n;  // nq
+};
+
 void search_on_replica(pag_gpu_index& ix, Replica& r, const pag_search_params& p, const float* q,
                        uint64_t nq, uint32_t* ids, float* sq, uint32_t* n_out,
-                       pag_search_stats* stats, uint32_t* status_or) {
+                       pag_search_stats* stats, uint32_t* status_or, const ConstructionHost* ch = nullptr) {
     cuda_check(cudaSetDevice(r.device), "cudaSetDevice");
     if (nq == 0) return;
     const uint32_t K = p.K;
-    const size_t qb = 4ull * nq * ix.dim;
+    const size_t qb = ch ? 4ull * nq : 4ull * nq * ix.dim;
     const size_t ob_ids = 4ull * nq * std::max(1u, K), ob_n = 4ull * nq,
                  ob_st = 4ull * nq * pagdev::kStatWords, ob_list = 4ull * nq;
+    const size_t ob_pes = ch ? 4ull * nq * ch->pes_cap : 0, ob_pn = ch ? 4ull * nq : 0;
     grow_dev(reinterpret_cast<void**>(&r.d_q), &r.d_q_bytes, qb);
-    grow_dev(reinterpret_cast<void**>(&r.d_out), &r.d_out_bytes, 2 * ob_ids + ob_n + ob_st + ob_list);
+    grow_dev(reinterpret_cast<void**>(&r.d_out), &r.d_out_bytes,
+             2 * ob_ids + ob_n + ob_st + ob_list + ob_pes + ob_pn);
     uint32_t* d_ids = reinterpret_cast<uint32_t*>(r.d_out);
     float* d_sq = reinterpret_cast<float*>(r.d_out + ob_ids);
     uint32_t* d_n = reinterpret_cast<uint32_t*>(r.d_out + 2 * ob_ids);
     uint32_t* d_st = reinterpret_cast<uint32_t*>(r.d_out + 2 * ob_ids + ob_n);
     uint32_t* d_list = reinterpret_cast<uint32_t*>(r.d_out + 2 * ob_ids + ob_n + ob_st);
-    cuda_check(cudaMemcpyAsync(r.d_q, q, qb, cudaMemcpyHostToDevice, r.stream), "H2D queries");
-    run_search(ix, r, p, r.d_q, static_cast<uint32_t>(nq), nullptr, d_ids, d_sq, d_n, d_st, r.stream, 0);
+    ConstructionArgs ca;
+    if (ch) {
+        ca.nodes = reinterpret_cast<const uint32_t*>(r.d_q);
+        ca.collect_pes = ch->collect_pes;
+        ca.pes_cap = ch->pes_cap;
+        ca.pes = reinterpret_cast<uint32_t*>(r.d_out + 2 * ob_ids + ob_n + ob_st + ob_list);
+        ca.pes_n = reinterpret_cast<uint32_t*>(r.d_out + 2 * ob_ids + ob_n + ob_st + ob_list + ob_pes);
+    }
+    const ConstructionArgs* cap = ch ? &ca : nullptr;
+    cuda_check(cudaMemcpyAsync(r.d_q, ch ? static_cast<const void*>(ch->nodes) : static_cast<const void*>(q), qb,
+                               cudaMemcpyHostToDevice, r.stream),
+               "H2D queries");
+    run_search(ix, r, p, r.d_q, static_cast<uint32_t>(nq), nullptr, d_ids, d_sq, d_n, d_st, r.stream, 0, cap);
     std::vector<uint32_t> st(nq * pagdev::kStatWords);
     cuda_check(cudaMemcpyAsync(st.data(), d_st, ob_st, cudaMemcpyDeviceToHost, r.stream), "D2H stats");
     cuda_check(cudaStreamSynchronize(r.stream), "search");
@@ -663,7 +700,7 @@ void search_on_replica(pag_gpu_index& ix, Replica& r, const pag_search_params& p
         cuda_check(cudaMemcpyAsync(d_list, redo.data(), 4 * redo.size(), cudaMemcpyHostToDevice, r.stream),
                    "H2D retry list");
         run_search(ix, r, p, r.d_q, static_cast<uint32_t>(redo.size()), d_list, d_ids, d_sq, d_n, d_st,
-                   r.stream, grow);
+                   r.stream, grow, cap);
         cuda_check(cudaMemcpyAsync(st.data(), d_st, ob_st, cudaMemcpyDeviceToHost, r.stream), "D2H stats");
         cuda_check(cudaStreamSynchronize(r.stream), "search retry");
     }
@@ -672,6 +709,10 @@ void search_on_replica(pag_gpu_index& ix, Replica& r, const pag_search_params& p
         cuda_check(cudaMemcpyAsync(sq, d_sq, 4ull * nq * K, cudaMemcpyDeviceToHost, r.stream), "D2H sq");
     }
     cuda_check(cudaMemcpyAsync(n_out, d_n, ob_n, cudaMemcpyDeviceToHost, r.stream), "D2H n_out");
+    if (ch) {
+        if (ob_pes) cuda_check(cudaMemcpyAsync(ch->pes, ca.pes, ob_pes, cudaMemcpyDeviceToHost, r.stream), "D2H pes");
+        cuda_check(cudaMemcpyAsync(ch->pes_n, ca.pes_n, ob_pn, cudaMemcpyDeviceToHost, r.stream), "D2H pes_n");
+    }
     cuda_check(cudaStreamSynchronize(r.stream), "D2H");
     uint32_t so = 0;
     for (uint64_t i = 0; i < nq; ++i) {
@@ -1042,10 +1083,11 @@ int pag_gpu_close(pag_gpu_index* ix) {
 int pag_gpu_info(const pag_gpu_index* ix, uint64_t* info, size_t n_info) {
     return guarded([&] {
         if (!ix || !info) throw_err(PAG_GPU_EINVAL, "null argument");
-        const uint64_t v[13] = {ix->n, ix->dim, ix->padded, ix->L, ix->m, ix->M, ix->metric,
+        const uint64_t v[16] = {ix->n, ix->dim, ix->padded, ix->L, ix->m, ix->M, ix->metric,
                                 ix->entries.size(), ix->seed, ix->total_edges, ix->reps.size(),
-                                ix->reps.empty() ? 0 : ix->reps[0].bytes, ix->gt_uncertified};
-        for (size_t i = 0; i < n_info && i < 13; ++i) info[i] = v[i];
+                                ix->reps.empty() ? 0 : ix->reps[0].bytes, ix->gt_uncertified,
+                                ix->efC, ix->b_build, ix->enable_pes};
+        for (size_t i = 0; i < n_info && i < 16; ++i) info[i] = v[i];
     });
 }
 
@@ -1084,6 +1126,60 @@ int pag_gpu_search(pag_gpu_index* ix, const float* q, uint64_t nq, const pag_sea
         for (auto s : status) so |= s;
         if (so & pagdev::kStatusZeroCosineQuery)
             throw_err(PAG_GPU_EINVAL, "zero query under cosine metric");
+        if (so & pagdev::kStatusVisitedOverflow)
+            throw_err(PAG_GPU_ERUNTIME, "visited set overflow after retries");
+    });
+}
+
+int pag_gpu_construction_search(pag_gpu_index* ix, const uint32_t* nodes, uint64_t nn,
+                                const pag_search_params* params, int collect_pes, uint32_t* ids, float* sq,
+                                uint32_t* n_out, pag_search_stats* stats, uint32_t* pes, uint32_t pes_cap,
+                                uint32_t* pes_n) {
+    return guarded([&] {
+        if (!ix) throw_err(PAG_GPU_EINVAL, "null argument");
+        std::lock_guard<std::mutex> g(ix->mu);
+        // insert_with_state (builder.cpp:220-224): K = efS = efC, b = b_build,
+        // collect_pes = enable_pes, unless the caller overrides
+        pag_search_params p{};
+        if (params) {
+            p = *params;
+        } else {
+            pag_gpu_default_params(&p);
+            p.K = p.efS = ix->efC;
+            p.b_override = ix->b_build;
+        }
+        const uint32_t pes_on = collect_pes < 0 ? ix->enable_pes : static_cast<uint32_t>(collect_pes != 0);
+        validate_params(*ix, p);
+        if (nn == 0) return;
+        if (!nodes || !n_out || !pes_n || (p.K && (!ids || !sq)) || (pes_cap && !pes))
+            throw_err(PAG_GPU_EINVAL, "null argument");
+        for (uint64_t i = 0; i < nn; ++i)
+            if (nodes[i] >= ix->n) throw_err(PAG_GPU_EINVAL, "node id out of range");
+        const size_t nd = ix->reps.size();
+        std::vector<uint32_t> status(nd, 0);
+        std::vector<PagError> errs;
+        std::mutex emu;
+        auto shard = [&](size_t d) {
+            const uint64_t q0 = nn * d / nd, q1 = nn * (d + 1) / nd;
+            ConstructionHost ch{nodes + q0, pes_on, pes_cap, pes ? pes + q0 * pes_cap : nullptr, pes_n + q0};
+            try {
+                search_on_replica(*ix, ix->reps[d], p, nullptr, q1 - q0, ids + q0 * p.K, sq + q0 * p.K,
+                                  n_out + q0, stats ? stats + q0 : nullptr, &status[d], &ch);
+            } catch (const PagError& e) {
+                std::lock_guard<std::mutex> lk(emu);
+                errs.push_back(e);
+            }
+        };
+        if (nd == 1) {
+            shard(0);
+        } else {
+            std::vector<std::thread> th;
+            for (size_t d = 0; d < nd; ++d) th.emplace_back(shard, d);
+            for (auto& t : th) t.join();
+        }
+        if (!errs.empty()) throw errs.front();
+        uint32_t so = 0;
+        for (auto s : status) so |= s;
         if (so & pagdev::kStatusVisitedOverflow)
             throw_err(PAG_GPU_ERUNTIME, "visited set overflow after retries");
     });

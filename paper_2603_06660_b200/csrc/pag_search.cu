@@ -118,7 +118,7 @@ struct Common {
     Arr rl, rl_tmp, mo;
     uint32_t rl_size, cap_r;
     // counters (routing.hpp:24-34 + edges_scanned)
-    uint32_t n_exact, n_test, n_pass, n_visited, n_edges;
+    uint32_t n_exact, n_test, n_pass, n_visited, n_edges, n_pes;
 #ifdef PAG_PHASE_TIMING
     long long pt_t0, pt_acc[8];
 #endif
@@ -1042,9 +1042,10 @@ __device__ __forceinline__ void prefetch_block_lanes(const IndexView& ix, uint32
     if (p && deg) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
-// routing.cpp:139-204 for W slot `slot`
+// routing.cpp:139-204 for W slot `slot`; returns out.pes_rejected
+// (always false unless P.collect_pes)
 template <class TFB, bool EXACT, int NCH>
-__device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, int lane) {
+__device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, int lane) {
     const IndexView& ix = P.ix;
     const float TAU_HI = 1.0f + 1e-6f;
     uint32_t u, deg;
@@ -1064,6 +1065,10 @@ __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
     c.n_edges += deg;
     const float duq = __fsqrt_rn(usq);
     const bool exact_mode = (duq == 0.0f) || !P.use_prt;
+    // PES margin (routing.cpp:150,190-199): rejected iff no edge reaches a
+    // margin >= 0 (pes_max starts at -inf; NaN margins never raise it)
+    const bool track_pes = P.collect_pes && duq > 0.0f;
+    bool pes_ok = false;
     const uint8_t* blk = ix.adj + static_cast<uint64_t>(u) * ix.block_bytes;
     const uint32_t S = ix.slot_stride;
     const uint32_t* tg = reinterpret_cast<const uint32_t*>(blk);
@@ -1109,7 +1114,7 @@ __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
         // (i) speculative PRT at the group-start radius
         const float adist0 = s.admission_dist();
         float quot = 0.0f, tau0 = 0.0f;
-        bool spec = false;
+        bool spec = false, have_quot = false;
         if (cand) {
             if (exact_mode) {
                 spec = true;
@@ -1120,9 +1125,21 @@ __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
                     const uint32_t* cp = cw_a + static_cast<uint64_t>(j) * ix.cwp;
                     const float sum = code_sum(c.T, ix.L, cp, ix.cwp, cw);
                     quot = __fdiv_rn(__fdiv_rn(__fsub_rn(sum, bo), duq), cbeta);
+                    have_quot = true;
                     spec = (tau <= -1.0f) || (quot >= tau);
                 }
             }
+        }
+        if (track_pes) {  // every edge, marked or not; quot does not depend on the radius
+            float x = -CUDART_INF_F;
+            if (active) {
+                if (!have_quot) {
+                    const uint32_t* cp = cw_a + static_cast<uint64_t>(j) * ix.cwp;
+                    quot = __fdiv_rn(__fdiv_rn(__fsub_rn(code_sum(c.T, ix.L, cp, ix.cwp, cw), bo), duq), cbeta);
+                }
+                x = __fsub_rn(quot, __fdiv_rn(en, __fmul_rn(2.0f, duq)));
+            }
+            pes_ok |= __any_sync(FULL, x >= 0.0f);
         }
         // (ii) compaction, (iii) exact distances of survivors
         const uint32_t surv = __ballot_sync(FULL, spec);
@@ -1182,6 +1199,7 @@ __device__ void expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
         PT(6);
         __syncwarp();
     }
+    return track_pes && !pes_ok;
 }
 
 template <class TFB, bool EXACT, int NCH>
@@ -1236,16 +1254,22 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
         c.gt_count = 0;
         c.gt_used = false;
         c.overflow = false;
-        c.n_exact = c.n_test = c.n_pass = c.n_visited = c.n_edges = 0;
+        c.n_exact = c.n_test = c.n_pass = c.n_visited = c.n_edges = c.n_pes = 0;
         s.reset();
         for (uint32_t i = lane; i < (1u << c.hs_log2); i += 32) c.hs[i] = EMPTY;
 
         // ---- query prep (routing.cpp:253-259): pad, cosine-normalise
-        const float* qraw = P.queries + static_cast<uint64_t>(qid) * ix.dim;
-        for (uint32_t k = lane; k < ix.dstride; k += 32) c.q[k] = (k < ix.dim) ? __ldg(qraw + k) : 0.0f;
-        __syncwarp();
         uint32_t status = 0;
-        if (ix.cosine) {
+        if (P.qnodes) {  // construction: the node's stored (padded, normalised) row as is
+            const float* row = ix.rows + static_cast<uint64_t>(P.qnodes[qid]) * ix.dstride;
+            for (uint32_t k = lane; k < ix.dstride; k += 32) c.q[k] = (k < ix.padded) ? __ldg(row + k) : 0.0f;
+            __syncwarp();
+        } else {
+            const float* qraw = P.queries + static_cast<uint64_t>(qid) * ix.dim;
+            for (uint32_t k = lane; k < ix.dstride; k += 32) c.q[k] = (k < ix.dim) ? __ldg(qraw + k) : 0.0f;
+            __syncwarp();
+        }
+        if (ix.cosine && !P.qnodes) {
             const float nrm = query_norm(c.q, ix.padded, lane);
             if (nrm == 0.0f) {
                 status |= kStatusZeroCosineQuery;
@@ -1349,7 +1373,12 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
             while (!c.overflow) {
                 const uint32_t i = s.next_unvisited(lane);
                 if (i == EMPTY) break;
-                expand<TFB, EXACT, NCH>(P, c, s, i, lane);
+                const uint32_t u = P.collect_pes ? s.entry_id(i) : 0u;
+                if (expand<TFB, EXACT, NCH>(P, c, s, i, lane)) {  // routing.cpp:235
+                    if (lane == 0 && c.n_pes < P.pes_cap)
+                        P.out_pes[static_cast<uint64_t>(qid) * P.pes_cap + c.n_pes] = u;
+                    ++c.n_pes;
+                }
             }
             PT(2);
             if (r + 1 == P.r_max || !s.end_round(c, lane)) break;
@@ -1380,6 +1409,7 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
             st[kStatStatus] = c.overflow ? kStatusVisitedOverflow : 0u;
             st[6] = c.hs_count + c.gt_count;  // marks held
             st[7] = c.gt_count;               // of which in the HBM bitmap
+            if (P.out_pes_n) P.out_pes_n[qid] = c.n_pes;
         }
         clear_bitmap(c, lane);
         __syncwarp();

@@ -79,6 +79,19 @@ class BatchResult:
                             SearchStats(*(int(x) for x in s)))
 
 
+@dataclass
+class ConstructionResult(BatchResult):
+    """BatchResult plus SearchResult.pes_rejected (routing.hpp:176) per node:
+    pes[i, :min(pes_n[i], pes_cap)] in expansion order."""
+    pes: np.ndarray = None     # nn x pes_cap uint32
+    pes_n: np.ndarray = None   # nn uint32 (full count)
+
+    def pes_rejected(self, i: int) -> List[int]:
+        if int(self.pes_n[i]) > self.pes.shape[1]:
+            raise RuntimeError("pes_rejected list truncated: raise pes_cap")
+        return [int(x) for x in self.pes[i, :int(self.pes_n[i])]]
+
+
 class PagIndex:
     """A PAGIDX01 index resident in HBM on one or more GPUs (move-only in the
     reference, builder.hpp:62-69; here a handle released by close())."""
@@ -89,10 +102,12 @@ class PagIndex:
             mask |= 1 << int(d)
         self._h = C.c_void_p()
         check(lib.pag_gpu_open(path.encode(), mask, C.byref(self._h)))
-        info = np.zeros(12, np.uint64)
-        check(lib.pag_gpu_info(self._h, info, 12))
+        info = np.zeros(16, np.uint64)
+        check(lib.pag_gpu_info(self._h, info, 16))
         (self.n, self.dim, self.padded_dim, self.L, self.m, self.M, metric, self.n_entries,
-         self.seed, self.total_edges, self.n_devices, self.device_bytes) = (int(x) for x in info)
+         self.seed, self.total_edges, self.n_devices, self.device_bytes, _, self.efC, self.b_build,
+         enable_pes) = (int(x) for x in info)
+        self.enable_pes = bool(enable_pes)
         self.metric = "cosine" if metric == 1 else "euclidean"
         self.path = path
 
@@ -143,6 +158,33 @@ class PagIndex:
                                  n_out.ctypes.data if nq else None, st))
         stats = np.ctypeslib.as_array(C.cast(st, C.POINTER(C.c_uint64)), (max(nq, 1), 5))[:nq].copy()
         return BatchResult(ids, sq, n_out, stats)
+
+    def construction_search(self, nodes, params: Optional[SearchParams] = None,
+                            collect_pes: Optional[bool] = None, pes_cap: int = 256) -> ConstructionResult:
+        """The search step of insert_with_state (builder.cpp:218-227) for
+        nodes already in the index: query = the node's stored row, K = efS =
+        efC, b = b_build, PES tracking per enable_pes (params / collect_pes
+        override). Returns results, counters and pes_rejected lists."""
+        nodes = np.ascontiguousarray(nodes, np.uint32).reshape(-1)
+        nn = len(nodes)
+        K = int(params.K) if params is not None else self.efC
+        ids = np.zeros((nn, K), np.uint32)
+        sq = np.zeros((nn, K), np.float32)
+        n_out = np.zeros(nn, np.uint32)
+        pes = np.zeros((nn, pes_cap), np.uint32)
+        pes_n = np.zeros(nn, np.uint32)
+        st = (SearchStatsC * max(nn, 1))()
+        pc = params.to_c() if params is not None else None
+        cp = -1 if collect_pes is None else int(bool(collect_pes))
+        check(lib.pag_gpu_construction_search(self._h, nodes.ctypes.data if nn else None, nn,
+                                              C.byref(pc) if pc is not None else None, cp,
+                                              ids.ctypes.data if K and nn else None,
+                                              sq.ctypes.data if K and nn else None,
+                                              n_out.ctypes.data if nn else None, st,
+                                              pes.ctypes.data if pes_cap and nn else None, pes_cap,
+                                              pes_n.ctypes.data if nn else None))
+        stats = np.ctypeslib.as_array(C.cast(st, C.POINTER(C.c_uint64)), (max(nn, 1), 5))[:nn].copy()
+        return ConstructionResult(ids, sq, n_out, stats, pes, pes_n)
 
     def search_device(self, q_ptr: int, nq: int, params: SearchParams, ids_ptr: int, sq_ptr: int,
                       n_out_ptr: int, stats_ptr: int, stream: int = 0) -> None:

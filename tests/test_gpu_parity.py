@@ -218,3 +218,47 @@ def test_single_query_api_and_empty_batch(pag, built):
     seeds = min(O.OracleIndex(fx["index"]).n_entries, 10)
     assert np.all(full.stats[:, 0] == seeds + full.stats[:, 2])
     assert np.all(full.stats[:, 1] >= full.stats[:, 2])
+
+
+CONSTRUCTION = [("euc48", {}), ("cos20", {}), ("deg64", {}), ("tail10", {}),
+                ("euc48", dict(K=50, efS=90, b_override=16)), ("euc48", dict(collect_pes=False)),
+                ("deg64", dict(K=64, efS=300, b_override=48))]
+
+
+@pytest.mark.parametrize("name,kw", CONSTRUCTION)
+def test_construction_search_bitexact(pag, built, name, kw):
+    """§8(f) next-2: insert_with_state's search (builder.cpp:218-227) batched
+    on the GPU — results, counters and pes_rejected lists (routing.cpp:190-199)
+    bit-identical to the oracle (b <= 32 register and b > 32 memory layouts)."""
+    fx = built(name)
+    ix = gpu_index(pag, fx["index"])
+    oix = O.OracleIndex(fx["index"])
+    nodes = np.arange(0, oix.n, 5, dtype=np.uint32)
+    params = None
+    if "K" in kw:
+        params = pag.SearchParams(K=kw["K"], efS=kw["efS"], b_override=kw["b_override"])
+    got = ix.construction_search(nodes, params, collect_pes=kw.get("collect_pes"))
+    want = oix.construction_search(nodes, **kw)
+    assert_same_results((got.ids, got.sq, got.n_out, got.stats), want[:4], f"construction {name} {kw}")
+    assert np.array_equal(got.pes_n, want[5])
+    for i in range(len(nodes)):
+        assert got.pes_rejected(i) == [int(x) for x in want[4][i, :int(want[5][i])]]
+    assert (got.pes_n.sum() > 0) == kw.get("collect_pes", True)
+
+
+def test_construction_search_vs_reference_binary_and_truncation(pag, built, fixture_dir):
+    fx = built("euc48")
+    ix = gpu_index(pag, fx["index"])
+    count, stride = 60, 41
+    ids, sq, n_out, st, pes, pes_n, _ = O.ref_build_search(fx["index"], count, stride,
+                                                          os.path.join(fixture_dir, "gbs.bin"), no_warm=True)
+    nodes = (np.arange(count, dtype=np.uint64) * stride % ix.n).astype(np.uint32)
+    got = ix.construction_search(nodes)
+    assert_same_results((got.ids, got.sq, got.n_out, got.stats[:, :4]), (ids, sq, n_out, st), "vs reference")
+    assert np.array_equal(got.pes_n, pes_n)
+    one = ix.construction_search(nodes, pes_cap=1)  # truncated lists keep the full count
+    assert np.array_equal(one.pes_n, pes_n)
+    has = pes_n > 0
+    assert np.array_equal(one.pes[has, 0], pes[has, 0])
+    with pytest.raises(ValueError, match="node id out of range"):
+        ix.construction_search(np.array([ix.n], np.uint32))

@@ -254,3 +254,34 @@ def test_recall_tie_policy_kat():  # test_bench.cpp:49-67
     r = lambda ids: O.recall_at_k(np.array(ids, np.uint32), t_ids, t_sq, 3)  # noqa: E731
     assert r([0, 1, 2]) == 1.0 and abs(r([0, 1, 42]) - 2 / 3) < 1e-12
     assert r([0, 1, 3]) == 1.0 and abs(r([0, 1, 4]) - 2 / 3) < 1e-12
+
+
+@pytest.mark.parametrize("name,kw", [("euc48", {}), ("cos20", {}), ("deg64", {}), ("tail10", {}),
+                                     ("euc48", dict(K=50, efS=90, b_override=16)),
+                                     ("euc48", dict(collect_pes=False))])
+def test_construction_search_matches_reference(built, fixture_dir, name, kw):
+    """insert_with_state's search (builder.cpp:218-227): the node's own row as
+    query, K = efS = efC, b = b_build, PES margins (routing.cpp:190-199) —
+    results, counters and the pes_rejected lists equal the reference's."""
+    fx = built(name)
+    ix = O.OracleIndex(fx["index"])
+    count, stride = 40, 37
+    nodes = (np.arange(count, dtype=np.uint64) * stride % ix.n).astype(np.uint32)
+    rkw = {}
+    if "K" in kw:
+        rkw.update(K=kw["K"], efS=kw["efS"], b=kw["b_override"])
+    if "collect_pes" in kw:
+        rkw["pes"] = int(kw["collect_pes"])
+    ids, sq, n_out, st, pes, pes_n, _ = O.ref_build_search(fx["index"], count, stride,
+                                                          os.path.join(fixture_dir, "bs.bin"), no_warm=True,
+                                                          **rkw)
+    gi, gs, gn, gst, gp, gpn = ix.construction_search(nodes, **kw)
+    assert_same_results((gi, gs, gn, gst[:, :4]), (ids, sq, n_out, st), f"construction {name} {kw}")
+    assert np.array_equal(gpn, pes_n)
+    for i in range(count):
+        m = min(int(pes_n[i]), pes.shape[1])
+        assert np.array_equal(gp[i, :m], pes[i, :m])
+    if kw.get("collect_pes", True):
+        assert pes_n.sum() > 0  # the fixture exercises the PES path
+    else:
+        assert pes_n.sum() == 0
