@@ -198,6 +198,8 @@ def main():
                          "other mode is also timed and compared")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="search", choices=["search", "construction"],
+                    help="construction: the search step of insert_with_state (SURVEY.md §8(f) next-2)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -223,6 +225,12 @@ def main():
         cfg, paths = prepare(args.config, args.cache_dir, threads)
     K = cfg["K"]
 
+    if args.mode == "construction":
+        if args.impl == "reference":
+            run_construction_reference(args, cfg, paths, rank, world, threads, dist)
+        else:
+            run_construction(args, cfg, paths, rank, world, local_rank, threads, dist)
+        return
     if args.impl == "reference":
         run_reference(args, cfg, paths, rank, world, threads, dist)
         return
@@ -552,6 +560,169 @@ def run_reference(args, cfg, paths, rank, world, threads, dist):
                                    f"(oracle/_ref/pag_ref) on {cpu_model()}"},
     }
     print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# construction search
+# ---------------------------------------------------------------------------
+CONS_STRIDE = 7919  # node i of a step = (i * 7919 + offset) % n (coprime to n: distinct nodes)
+
+
+def cons_nodes(n: int, count: int, offset: int = 0) -> np.ndarray:
+    return ((np.arange(count, dtype=np.uint64) * CONS_STRIDE + offset) % n).astype(np.uint32)
+
+
+def cpu_construction(index_path: str, threads: int, count: int, reps: int):
+    out = subprocess.run([REF_BIN, "build-search", f"--index={index_path}", f"--count={count}",
+                          f"--stride={CONS_STRIDE}", f"--threads={threads}", f"--reps={reps}"],
+                         check=True, capture_output=True, text=True)
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def run_construction(args, cfg, paths, rank, world, local_rank, threads, dist):
+    """The search step of insert_with_state (builder.cpp:218-227) for a batch
+    of existing nodes: query = the node's stored row, K = efS = efC, b =
+    b_build, PES margins collected (header defaults of the reference build).
+    The headline uses reference-order (bit-identical) distances, since the
+    build's graph depends on every bit; warp-tree is timed beside it."""
+    import torch
+
+    import paper_2603_06660_b200 as pag
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    ix = pag.load_index(paths["index"], devices=(local_rank,))
+    nn, cap = cfg["nq"], 256
+    K = ix.efC
+    nodes = cons_nodes(ix.n, nn * world)[rank * nn:(rank + 1) * nn]  # disjoint node shards
+    modes = {}
+    nodes_d = torch.from_numpy(nodes.view(np.int32)).to(dev)
+    bufs = [torch.empty((nn, K), dtype=torch.int32, device=dev), torch.empty((nn, K), dtype=torch.float32, device=dev),
+            torch.empty((nn,), dtype=torch.int32, device=dev), torch.empty((nn, 8), dtype=torch.int32, device=dev),
+            torch.empty((nn, cap), dtype=torch.int32, device=dev), torch.empty((nn,), dtype=torch.int32, device=dev)]
+    stream = torch.cuda.Stream(dev)
+    clk_summary = None
+    for mode in ("exact", "warp-tree"):
+        params = pag.SearchParams(K=K, efS=K, b_override=ix.b_build, exact_dist=mode == "exact")
+
+        def step():
+            ix.construction_search_device(nodes_d.data_ptr(), nn, params, None, bufs[0].data_ptr(),
+                                          bufs[1].data_ptr(), bufs[2].data_ptr(), bufs[3].data_ptr(),
+                                          bufs[4].data_ptr(), cap, bufs[5].data_ptr(), stream.cuda_stream)
+        for _ in range(max(3, args.warmup)):
+            step()
+        torch.cuda.synchronize(dev)
+        if dist is not None:
+            dist.barrier()
+        steps = args.steps if mode == "exact" else max(3, min(args.steps, 5))
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        with Clocks(local_rank) as clk:
+            ev[0].record(stream)
+            for _ in range(steps):
+                step()
+            ev[1].record(stream)
+            torch.cuda.synchronize(dev)
+        if mode == "exact":
+            clk_summary = clk.summary()
+        ms = max_over_ranks(ev[0].elapsed_time(ev[1]), dist, dev)
+        st = bufs[3].cpu().numpy().view(np.uint32).astype(np.uint64)
+        modes[mode] = {"ms": ms, "steps": steps, "stats": st, "ids": bufs[0].cpu().numpy().view(np.uint32).copy(),
+                       "n": bufs[2].cpu().numpy().view(np.uint32).copy(),
+                       "pes_n": bufs[5].cpu().numpy().view(np.uint32).copy()}
+    m = modes["exact"]
+    value = world * nn * m["steps"] / (m["ms"] / 1e3)
+    w = modes["warp-tree"]
+    same = float(np.mean([set(m["ids"][i, :m["n"][i]].tolist()) == set(w["ids"][i, :w["n"][i]].tolist())
+                          for i in range(nn)]))
+    bytes_total = algorithmic_bytes(m["stats"][:, [0, 1, 2, 3, 4]], ix.padded_dim, ix.L, K)
+    achieved = bytes_total / (m["ms"] / m["steps"] / 1e3) / 1e9
+    peak, peak_kind = load_peaks()
+    # e2e: host node ids in, host results + PES lists out, through the C ABI
+    e2e_steps = 0 if args.no_e2e else max(3, min(args.steps, 10))
+    hp = pag.SearchParams(K=K, efS=K, b_override=ix.b_build)
+    for _ in range(1 if e2e_steps else 0):
+        ix.construction_search(nodes, hp, pes_cap=cap)
+    if dist is not None:
+        dist.barrier()
+    t = time.perf_counter()
+    for _ in range(e2e_steps):
+        ix.construction_search(nodes, hp, pes_cap=cap)
+    e2e_s = max_over_ranks(max(time.perf_counter() - t, 1e-9), dist, dev)
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline and os.path.exists(REF_BIN):
+        lim = min(nn, 2000)
+        c = cpu_construction(paths["index"], threads, lim, 2)
+        cpu = {"value": round(c["qps"], 1), "unit": "construction searches/s", "cores": threads,
+               "kind": "reference",
+               "sample": f"first {lim} nodes of the same node sequence x 2 timed sweeps after 1 warm sweep, "
+                         f"reference search_padded with collect_pes (oracle/_ref/pag_ref build-search), "
+                         f"{threads} threads on {cpu_model()}"}
+    sm = m["stats"].astype(np.float64)
+    line = {
+        "metric": f"construction searches/s (insert_with_state search: K=efS=efC={K}, b=b_build={ix.b_build}, "
+                  f"PES, {cfg['n']}x{cfg['d']})",
+        "value": round(value, 1), "unit": "construction searches/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": round(m["ms"] / m["steps"], 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded Gaussian mixture per BASELINE.json; index from the reference CPU build)",
+        "config": {"workload": f"{args.config}-construction", "n": cfg["n"], "d": cfg["d"],
+                   "nodes_per_step": nn, "node_sequence": f"(i * {CONS_STRIDE}) % n", "K": K, "efS": K,
+                   "b": ix.b_build, "collect_pes": bool(ix.enable_pes), "pes_cap": cap,
+                   "distance_mode": "exact (bit-identical to the reference)",
+                   "other_mode": {"distance_mode": "warp-tree",
+                                  "value": round(world * nn * w["steps"] / (w["ms"] / 1e3), 1),
+                                  "id_sets_equal_frac": round(same, 5)},
+                   "l2": "index (>3 GB) exceeds the 126 MB L2; no flush needed",
+                   "parallelism": f"node shards, index replica per GPU x{world}"},
+        "e2e": {"value": round(world * nn * e2e_steps / e2e_s, 1), "unit": "construction searches/s",
+                "h2d_bytes_per_step": nn * 4, "d2h_bytes_per_step": nn * (8 * K + 4 + 4 * 5 + 4 + 4 * cap)},
+        "gpu_launches": args.steps,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind,
+                     "bytes_per_query": round(bytes_total / nn, 1),
+                     "algorithmic_bytes_per_launch": round(bytes_total, 1)},
+        "per_node": {"exact": round(float(sm[:, 0].mean()), 2), "tests": round(float(sm[:, 1].mean()), 2),
+                     "passes": round(float(sm[:, 2].mean()), 2), "expansions": round(float(sm[:, 3].mean()), 2),
+                     "edges_scanned": round(float(sm[:, 4].mean()), 2),
+                     "pes_rejected": round(float(m["pes_n"].mean()), 3)},
+        "clocks": clk_summary,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def run_construction_reference(args, cfg, paths, rank, world, threads, dist):
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    lim = min(cfg["nq"], 2000)
+    c = cpu_construction(paths["index"], threads, lim, max(1, args.steps))
+    unit = "construction searches/s"
+    print(json.dumps({
+        "impl": "reference",
+        "metric": f"construction searches/s (insert_with_state search, {cfg['n']}x{cfg['d']})",
+        "value": round(c["qps"], 1), "unit": unit, "n_gpus": world, "steps": args.steps, "warmup": 1,
+        "ms_per_step": round(1e3 * c["seconds_mean"], 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded Gaussian mixture per BASELINE.json; index from the reference CPU build)",
+        "config": {"workload": f"{args.config}-construction", "nodes_per_step": lim,
+                   "node_sequence": f"(i * {CONS_STRIDE}) % n", "parallelism": f"{threads} host threads"},
+        "e2e": {"value": round(c["qps"], 1), "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": round(c["qps"], 1), "unit": unit, "cores": threads, "kind": "reference",
+                         "sample": f"first {lim} nodes per step, 1 warm sweep, reference search_padded with "
+                                   f"collect_pes (oracle/_ref/pag_ref build-search) on {cpu_model()}"},
+    }), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()

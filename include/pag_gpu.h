@@ -124,6 +124,15 @@ int pag_gpu_construction_search(pag_gpu_index* ix, const uint32_t* nodes, uint64
                                 uint32_t* n_out, pag_search_stats* stats, uint32_t* pes, uint32_t pes_cap,
                                 uint32_t* pes_n);
 
+/* pag_gpu_construction_search with every buffer on device 0 of the handle
+ * (node ids must be < n; not checked here), launched on `stream` without
+ * host synchronisation; stats_dev: nn x 8 u32 raw counters as
+ * pag_gpu_search_device. No visited-overflow retry on this path. */
+int pag_gpu_construction_search_device(pag_gpu_index* ix, const uint32_t* nodes_dev, uint64_t nn,
+                                       const pag_search_params* params, int collect_pes, uint32_t* ids_dev,
+                                       float* sq_dev, uint32_t* n_out_dev, uint32_t* stats_dev,
+                                       uint32_t* pes_dev, uint32_t pes_cap, uint32_t* pes_n_dev, void* stream);
+
 /* Replaces: GroundTruth ground_truth(const VectorSet& base,
  *                                    const VectorSet& queries, uint32_t k_star)
  *           proj/include/pag/bench.hpp:19, proj/src/bench.cpp:18-53,

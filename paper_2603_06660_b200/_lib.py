@@ -30,6 +30,7 @@ EXPORTS = (
     "pag_gpu_search",
     "pag_gpu_search_device",
     "pag_gpu_construction_search",
+    "pag_gpu_construction_search_device",
     "pag_gpu_ground_truth",
     "pag_gpu_refresh",
     "pag_gpu_inspect",
@@ -75,6 +76,9 @@ def _load():
         "pag_gpu_construction_search": (C.c_int, [P, C.c_void_p, C.c_uint64, C.c_void_p, C.c_int,
                                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                                   C.c_void_p, C.c_uint32, C.c_void_p]),
+        "pag_gpu_construction_search_device": (C.c_int, [P, C.c_void_p, C.c_uint64, C.c_void_p, C.c_int,
+                                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                         C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
         "pag_gpu_ground_truth": (C.c_int, [P, f32p, C.c_uint64, C.c_uint32, u32p, f32p]),
         "pag_gpu_refresh": (C.c_int, [P, C.c_char_p, u64p]),
         "pag_gpu_inspect": (C.c_int, [C.c_char_p, u64p, C.c_size_t]),

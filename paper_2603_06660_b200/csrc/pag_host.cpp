@@ -714,6 +714,9 @@ void search_on_replica(pag_gpu_index& ix, Replica& r, const pag_search_params& p
         cuda_check(cudaMemcpyAsync(ch->pes_n, ca.pes_n, ob_pn, cudaMemcpyDeviceToHost, r.stream), "D2H pes_n");
     }
     cuda_check(cudaStreamSynchronize(r.stream), "D2H");
+    if (ch && ch->pes_cap)  // entries past each list are unspecified on the device: zero them
+        for (uint64_t i = 0; i < nq; ++i)
+            for (uint32_t j = std::min(ch->pes_n[i], ch->pes_cap); j < ch->pes_cap; ++j) ch->pes[i * ch->pes_cap + j] = 0;
     uint32_t so = 0;
     for (uint64_t i = 0; i < nq; ++i) {
         const uint32_t* s = &st[i * pagdev::kStatWords];
@@ -1182,6 +1185,36 @@ int pag_gpu_construction_search(pag_gpu_index* ix, const uint32_t* nodes, uint64
         for (auto s : status) so |= s;
         if (so & pagdev::kStatusVisitedOverflow)
             throw_err(PAG_GPU_ERUNTIME, "visited set overflow after retries");
+    });
+}
+
+int pag_gpu_construction_search_device(pag_gpu_index* ix, const uint32_t* nodes_dev, uint64_t nn,
+                                       const pag_search_params* params, int collect_pes, uint32_t* ids_dev,
+                                       float* sq_dev, uint32_t* n_out_dev, uint32_t* stats_dev,
+                                       uint32_t* pes_dev, uint32_t pes_cap, uint32_t* pes_n_dev, void* stream) {
+    return guarded([&] {
+        if (!ix) throw_err(PAG_GPU_EINVAL, "null argument");
+        std::lock_guard<std::mutex> g(ix->mu);
+        pag_search_params p{};
+        if (params) {
+            p = *params;
+        } else {
+            pag_gpu_default_params(&p);
+            p.K = p.efS = ix->efC;
+            p.b_override = ix->b_build;
+        }
+        validate_params(*ix, p);
+        if (nn >= 0xFFFFFFFFull) throw_err(PAG_GPU_EINVAL, "batch too large");
+        Replica& r = ix->reps[0];
+        cuda_check(cudaSetDevice(r.device), "cudaSetDevice");
+        ConstructionArgs ca;
+        ca.nodes = nodes_dev;
+        ca.collect_pes = collect_pes < 0 ? ix->enable_pes : static_cast<uint32_t>(collect_pes != 0);
+        ca.pes_cap = pes_cap;
+        ca.pes = pes_dev;
+        ca.pes_n = pes_n_dev;
+        run_search(*ix, r, p, nullptr, static_cast<uint32_t>(nn), nullptr, ids_dev, sq_dev, n_out_dev, stats_dev,
+                   static_cast<cudaStream_t>(stream), 0, &ca);
     });
 }
 

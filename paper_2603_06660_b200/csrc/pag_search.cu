@@ -35,6 +35,10 @@
 
 #include "pag_device.h"
 
+#ifndef PAG_PES
+#define PAG_PES 0
+#endif
+
 namespace pagdev {
 namespace {
 
@@ -1043,8 +1047,8 @@ __device__ __forceinline__ void prefetch_block_lanes(const IndexView& ix, uint32
 }
 
 // routing.cpp:139-204 for W slot `slot`; returns out.pes_rejected
-// (always false unless P.collect_pes)
-template <class TFB, bool EXACT, int NCH>
+// (always false unless PES: the construction search with collect_pes)
+template <class TFB, bool EXACT, int NCH, bool PES>
 __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, int lane) {
     const IndexView& ix = P.ix;
     const float TAU_HI = 1.0f + 1e-6f;
@@ -1067,7 +1071,7 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
     const bool exact_mode = (duq == 0.0f) || !P.use_prt;
     // PES margin (routing.cpp:150,190-199): rejected iff no edge reaches a
     // margin >= 0 (pes_max starts at -inf; NaN margins never raise it)
-    const bool track_pes = P.collect_pes && duq > 0.0f;
+    const bool track_pes = PES && duq > 0.0f;
     bool pes_ok = false;
     const uint8_t* blk = ix.adj + static_cast<uint64_t>(u) * ix.block_bytes;
     const uint32_t S = ix.slot_stride;
@@ -1202,7 +1206,7 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
     return track_pes && !pes_ok;
 }
 
-template <class TFB, bool EXACT, int NCH>
+template <class TFB, bool EXACT, int NCH, bool PES>
 #ifndef PAG_MIN_BLOCKS
 #define PAG_MIN_BLOCKS 4
 #endif
@@ -1373,8 +1377,8 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
             while (!c.overflow) {
                 const uint32_t i = s.next_unvisited(lane);
                 if (i == EMPTY) break;
-                const uint32_t u = P.collect_pes ? s.entry_id(i) : 0u;
-                if (expand<TFB, EXACT, NCH>(P, c, s, i, lane)) {  // routing.cpp:235
+                const uint32_t u = PES ? s.entry_id(i) : 0u;
+                if (expand<TFB, EXACT, NCH, PES>(P, c, s, i, lane)) {  // routing.cpp:235
                     if (lane == 0 && c.n_pes < P.pes_cap)
                         P.out_pes[static_cast<uint64_t>(qid) * P.pes_cap + c.n_pes] = u;
                     ++c.n_pes;
@@ -1422,7 +1426,7 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
 
 template <class TFB, bool EXACT, int NCH>
 cudaError_t launch_t(const SearchLaunch& L, int grid, size_t smem, cudaStream_t stream, int* bps) {
-    auto k = pag_search_kernel<TFB, EXACT, NCH>;
+    auto k = pag_search_kernel<TFB, EXACT, NCH, PAG_PES != 0>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     if (bps) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k, L.warps_per_block * 32, smem);
@@ -1443,7 +1447,7 @@ cudaError_t dispatch_nch(const SearchLaunch& L, int grid, size_t smem, cudaStrea
     }
 }
 
-cudaError_t dispatch(const SearchLaunch& L, int grid, cudaStream_t stream, int* bps) {
+cudaError_t dispatch_tfb(const SearchLaunch& L, int grid, cudaStream_t stream, int* bps) {
     const size_t smem = static_cast<size_t>(L.warp_smem_bytes) * L.warps_per_block;
     if (L.b <= 32)
         return L.exact_dist ? dispatch_nch<TfbReg, true>(L, grid, smem, stream, bps)
@@ -1452,6 +1456,21 @@ cudaError_t dispatch(const SearchLaunch& L, int grid, cudaStream_t stream, int* 
                         : dispatch_nch<TfbMem, false>(L, grid, smem, stream, bps);
 }
 
+}  // namespace
+
+#if PAG_PES
+// construction-search instantiations (this file compiled again with
+// -DPAG_PES=1, keeping the PES code out of the query kernels)
+cudaError_t dispatch_pes(const SearchLaunch& L, int grid, cudaStream_t stream, int* bps) {
+    return dispatch_tfb(L, grid, stream, bps);
+}
+#else
+cudaError_t dispatch_pes(const SearchLaunch& L, int grid, cudaStream_t stream, int* bps);
+
+namespace {
+cudaError_t dispatch(const SearchLaunch& L, int grid, cudaStream_t stream, int* bps) {
+    return L.collect_pes ? dispatch_pes(L, grid, stream, bps) : dispatch_tfb(L, grid, stream, bps);
+}
 }  // namespace
 
 size_t search_kernel_smem(const SearchLaunch& L) {
@@ -1478,5 +1497,6 @@ cudaError_t search_occupancy(const SearchLaunch& L, int* blocks_per_sm) { return
 cudaError_t launch_search(const SearchLaunch& L, int grid, cudaStream_t stream) {
     return dispatch(L, grid, stream, nullptr);
 }
+#endif  // PAG_PES
 
 }  // namespace pagdev

@@ -186,6 +186,17 @@ class PagIndex:
         stats = np.ctypeslib.as_array(C.cast(st, C.POINTER(C.c_uint64)), (max(nn, 1), 5))[:nn].copy()
         return ConstructionResult(ids, sq, n_out, stats, pes, pes_n)
 
+    def construction_search_device(self, nodes_ptr: int, nn: int, params: Optional[SearchParams],
+                                   collect_pes: Optional[bool], ids_ptr: int, sq_ptr: int, n_out_ptr: int,
+                                   stats_ptr: int, pes_ptr: int, pes_cap: int, pes_n_ptr: int,
+                                   stream: int = 0) -> None:
+        """Device-resident construction batch (async on `stream`)."""
+        pc = params.to_c() if params is not None else None
+        cp = -1 if collect_pes is None else int(bool(collect_pes))
+        check(lib.pag_gpu_construction_search_device(self._h, nodes_ptr, nn, C.byref(pc) if pc is not None else None,
+                                                     cp, ids_ptr, sq_ptr, n_out_ptr, stats_ptr, pes_ptr, pes_cap,
+                                                     pes_n_ptr, stream or None))
+
     def search_device(self, q_ptr: int, nq: int, params: SearchParams, ids_ptr: int, sq_ptr: int,
                       n_out_ptr: int, stats_ptr: int, stream: int = 0) -> None:
         """Device-resident batch (pointers on the handle's first GPU); async

@@ -22,7 +22,7 @@ def _ensure_built():
     subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "-s"], check=True)
     so = os.path.join(ROOT, "paper_2603_06660_b200", "libpag_gpu.so")
     if not os.path.exists(so):
-        subprocess.run(["make", "-C", os.path.join(ROOT, "paper_2603_06660_b200", "csrc"), "-s"], check=True)
+        subprocess.run(["make", "-C", os.path.join(ROOT, "paper_2603_06660_b200", "csrc"), "-s", "-j4"], check=True)
 
 
 _ensure_built()

@@ -262,3 +262,26 @@ def test_construction_search_vs_reference_binary_and_truncation(pag, built, fixt
     assert np.array_equal(one.pes[has, 0], pes[has, 0])
     with pytest.raises(ValueError, match="node id out of range"):
         ix.construction_search(np.array([ix.n], np.uint32))
+
+
+def test_construction_device_path_matches_host_path(pag, built):
+    import torch
+    fx = built("deg64")
+    ix = gpu_index(pag, fx["index"])
+    nodes = np.arange(0, ix.n, 11, dtype=np.uint32)
+    host = ix.construction_search(nodes)
+    nn, K, cap = len(nodes), ix.efC, 256
+    d = lambda *s, t=torch.int32: torch.zeros(s, dtype=t, device="cuda")  # noqa: E731
+    nodes_d = torch.from_numpy(nodes.view(np.int32)).cuda()
+    ids, sq, n, st, pes, pn = d(nn, K), d(nn, K, t=torch.float32), d(nn), d(nn, 8), d(nn, cap), d(nn)
+    ix.construction_search_device(nodes_d.data_ptr(), nn, None, None, ids.data_ptr(), sq.data_ptr(), n.data_ptr(),
+                                  st.data_ptr(), pes.data_ptr(), cap, pn.data_ptr(),
+                                  torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(ids.cpu().numpy().view(np.uint32), host.ids)
+    assert np.array_equal(sq.cpu().numpy(), host.sq)
+    assert np.array_equal(pn.cpu().numpy().view(np.uint32), host.pes_n)
+    pes = pes.cpu().numpy().view(np.uint32)
+    for i in range(nn):  # entries past pes_n are unspecified on the device path
+        m = min(int(host.pes_n[i]), cap)
+        assert np.array_equal(pes[i, :m], host.pes[i, :m])
