@@ -90,6 +90,8 @@ struct SearchLaunch {
 };
 
 size_t search_kernel_smem(const SearchLaunch& L);
+// kernels bounded for 6 resident blocks per SM (large efS) instead of 4
+bool search_high_occupancy(const SearchLaunch& L);
 // b <= 32: working set and rings in registers (no smem for them)
 bool search_uses_registers(const SearchLaunch& L);
 cudaError_t launch_search(const SearchLaunch& L, int grid, cudaStream_t stream);

@@ -524,7 +524,10 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     L.warps_per_block = kWarpsPerBlock;
     L.tune = std::getenv("PAG_GPU_TUNE") ? static_cast<uint32_t>(std::atoi(std::getenv("PAG_GPU_TUNE"))) : 0u;
     L.stage_rows = 4;
-    L.hash_log2 = p.efS <= 200 ? 10 : 11;
+    // the visited hash holds ~half its slots before spilling to the bitmap:
+    // 512 marks cover efS <= 200 at K = 10; past that the marks outgrow any
+    // on-chip table and a small one keeps occupancy (W is on-chip)
+    L.hash_log2 = p.efS <= 200 ? 10 : 8;
     if (const char* e = std::getenv("PAG_GPU_HASH_LOG2")) L.hash_log2 = static_cast<uint32_t>(std::atoi(e));
     const uint32_t b = L.b;
     L.rl_cap = L.r_max * b + b;  // every W flush of a query (r_max - 1 end_rounds + the final flush)
@@ -551,12 +554,17 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     auto total = [&]() {
         return off + (w_s ? szW : 0) + (r_s ? szR : 0) + (rl_s ? szRL : 0) + (m_s ? szM : 0);
     };
-    if (total() > kWarpSmemBudget) rl_s = false;
-    if (total() > kWarpSmemBudget) m_s = false;
-    if (total() > kWarpSmemBudget) r_s = false;
-    // the working set is scanned on every expansion: keep it on-chip even at
-    // the cost of occupancy (large b), up to 48 KB per warp
-    if (total() > std::max<uint64_t>(kWarpSmemBudget, std::min<uint64_t>(48 * 1024, off + szW))) w_s = false;
+    // per-warp budget that keeps the kernel's resident-block bound (4 or 6
+    // blocks of 4 warps in 228 KB) reachable
+    const uint64_t budget = pagdev::search_high_occupancy(L) ? std::min<uint32_t>(kWarpSmemBudget, 9 * 1024)
+                                                             : kWarpSmemBudget;
+    if (total() > budget) rl_s = false;
+    if (total() > budget) m_s = false;
+    if (total() > budget) r_s = false;
+    // W last: with the per-owner caches it is touched S = b/32 entries at a
+    // time (L1-friendly), and occupancy (4 blocks/SM) hides more latency
+    // than an on-chip W saves (cfg4 K=1000: +17%)
+    if (total() > budget) w_s = false;
     uint64_t goff = 0;
     auto place = [&](bool in_smem, uint64_t sz, uint32_t* o, uint32_t* flag) {
         *flag = in_smem;

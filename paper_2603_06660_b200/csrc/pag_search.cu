@@ -31,12 +31,24 @@
 // R_L (capacity efS) is an array in smem, or HBM when it does not fit.
 #include <cuda_runtime.h>
 #include <math_constants.h>
+#include <stdlib.h>
 #include <stdint.h>
 
 #include "pag_device.h"
 
+// Build flavours of this file (csrc/Makefile compiles it four times):
+//   PAG_PES   0/1  query kernels / construction kernels with PES tracking
+//   PAG_OCC   4/6  resident blocks of 4 warps per SM the kernels are
+//                  register-bounded for: 4 (128 regs) for the usual
+//                  operating points, 6 (80 regs) for large efS, where the
+//                  visited set lives mostly in the HBM bitmap and latency
+//                  hiding (more warps) pays more than registers
+// The (PES 0, OCC 4) object holds the public entry points and dispatches.
 #ifndef PAG_PES
 #define PAG_PES 0
+#endif
+#ifndef PAG_OCC
+#define PAG_OCC 4
 #endif
 
 namespace pagdev {
@@ -463,64 +475,104 @@ struct TfbReg {
 // ---------------------------------------------------------------------------
 // TfbMem: b > 32. Arrays in smem or the warp's HBM slot.
 // ---------------------------------------------------------------------------
+// b > 32: W and the rings as arrays (smem, or the warp's HBM slot). Lane o
+// owns the contiguous W slots [o*S, o*S+S), S = ceil(b/32), and caches in
+// registers the best unvisited (sq, id) and the largest sq (lowest slot on
+// ties) of its slots. argmin / argmax are then one warp reduction over the
+// caches; a change to a slot re-scans only its owner's S slots, all lanes
+// reading consecutive slots (conflict-free). Same selections as the full
+// scans of routing.cpp:32-44,71-80.
 struct TfbMem {
     Arr W, rf, rt, mi;
-    uint32_t b;
+    uint32_t b, S;
     uint32_t wsize, rf_head, rf_size, rt_head, rt_size;
     float zmax_sq, zmax_dist;
     uint32_t zmax_idx;
+    // this lane's caches over its slots
+    uint32_t mn_key, mn_id, mn_slot;  // best unvisited by (sq, id); mn_slot EMPTY if none
+    uint32_t mx_key, mx_slot;         // largest sq, lowest slot; mx_slot EMPTY if none
 
     __device__ void init(uint32_t b_, uint8_t* sw, uint8_t* gw, const SearchLaunch& P) {
         b = b_;
+        S = (b + 31) / 32;
         W = make_arr((P.W_in_smem ? sw : gw) + P.off_W, b);
         rf = make_arr((P.rings_in_smem ? sw : gw) + P.off_rf, b);
         rt = make_arr((P.rings_in_smem ? sw : gw) + P.off_rt, b);
         mi = make_arr((P.merge_in_smem ? sw : gw) + P.off_merge, 2 * b);
     }
+    __device__ void clear_caches() {
+        mn_key = mn_id = 0xffffffffu;
+        mn_slot = mx_slot = EMPTY;
+        mx_key = 0;
+    }
     __device__ void reset() {
         wsize = rf_head = rf_size = rt_head = rt_size = 0;
         zmax_sq = zmax_dist = 0.0f;
         zmax_idx = 0;
+        clear_caches();
     }
     __device__ float admission_sq() const { return wsize < b ? CUDART_INF_F : zmax_sq; }
     __device__ float admission_dist() const { return wsize < b ? CUDART_INF_F : zmax_dist; }
 
-    __device__ void recompute_zmax(int lane) {
+    // re-derive owner o's caches from its slots (warp-cooperative)
+    __device__ void rescan(uint32_t o, int lane) {
+        uint32_t nk = 0xffffffffu, ni = 0xffffffffu, ns = EMPTY, xk = 0, xs = EMPTY;
+        for (uint32_t j = lane; j < S; j += 32) {
+            const uint32_t i = o * S + j;
+            if (i >= wsize) break;
+            const uint32_t k = fkey(W.sq[i]);
+            if (xs == EMPTY || k > xk) {
+                xk = k;
+                xs = i;
+            }
+            if (!(W.aux[i] & VISITED)) {
+                const uint32_t id = W.id[i];
+                if (ns == EMPTY || k < nk || (k == nk && id < ni)) {
+                    nk = k;
+                    ni = id;
+                    ns = i;
+                }
+            }
+        }
+        const uint32_t m1 = __reduce_min_sync(FULL, ns == EMPTY ? 0xffffffffu : nk);
+        const bool c1 = ns != EMPTY && nk == m1;
+        const uint32_t m2 = __reduce_min_sync(FULL, c1 ? ni : 0xffffffffu);
+        const uint32_t s1 = __reduce_min_sync(FULL, (c1 && ni == m2) ? ns : EMPTY);
+        const uint32_t x1 = __reduce_max_sync(FULL, xs == EMPTY ? 0u : xk);
+        const uint32_t xs1 = __reduce_min_sync(FULL, (xs != EMPTY && xk == x1) ? xs : EMPTY);
+        if (static_cast<uint32_t>(lane) == o) {
+            mn_key = m1;
+            mn_id = m2;
+            mn_slot = s1;
+            mx_key = x1;
+            mx_slot = xs1;
+        }
+    }
+    // routing.cpp:32-44 from the caches: argmax, first slot on ties
+    __device__ void zmax_from_caches() {
+        const uint32_t m = __reduce_max_sync(FULL, mx_slot == EMPTY ? 0u : mx_key);
+        zmax_idx = __reduce_min_sync(FULL, (mx_slot != EMPTY && mx_key == m) ? mx_slot : EMPTY);
+        zmax_sq = W.sq[zmax_idx];
+        zmax_dist = __fsqrt_rn(zmax_sq);
+    }
+    __device__ void recompute_zmax(int lane) {  // after a wholesale refill of W
+        clear_caches();
         if (wsize == 0) {
             zmax_sq = zmax_dist = 0.0f;
             zmax_idx = 0;
             return;
         }
-        uint32_t bk = 0, bi = EMPTY;
-        for (uint32_t i = lane; i < wsize; i += 32) {
-            const uint32_t k = fkey(W.sq[i]);
-            if (bi == EMPTY || k > bk) {
-                bk = k;
-                bi = i;
-            }
-        }
-        const uint32_t m = __reduce_max_sync(FULL, bi == EMPTY ? 0u : bk);
-        zmax_idx = __reduce_min_sync(FULL, (bi != EMPTY && bk == m) ? bi : EMPTY);
-        zmax_sq = W.sq[zmax_idx];
-        zmax_dist = __fsqrt_rn(zmax_sq);
+        const uint32_t owners = (wsize + S - 1) / S;
+        for (uint32_t o = 0; o < owners; ++o) rescan(o, lane);
+        zmax_from_caches();
     }
-    __device__ uint32_t next_unvisited(int lane, uint32_t skip = EMPTY) const {
-        uint32_t bk = 0xffffffffu, bid = EMPTY, bslot = EMPTY;
-        for (uint32_t i = lane; i < wsize; i += 32) {
-            if ((W.aux[i] & VISITED) || i == skip) continue;
-            const uint32_t k = fkey(W.sq[i]);
-            const uint32_t id = W.id[i];
-            if (bslot == EMPTY || k < bk || (k == bk && id < bid)) {
-                bk = k;
-                bid = id;
-                bslot = i;
-            }
-        }
-        const uint32_t m1 = __reduce_min_sync(FULL, bslot == EMPTY ? 0xffffffffu : bk);
-        const bool c1 = bslot != EMPTY && bk == m1;
-        if (!__ballot_sync(FULL, bslot != EMPTY)) return EMPTY;
-        const uint32_t m2 = __reduce_min_sync(FULL, c1 ? bid : 0xffffffffu);
-        return __reduce_min_sync(FULL, (c1 && bid == m2) ? bslot : EMPTY);
+    // routing.cpp:71-80: argmin over unvisited by (sq, id)
+    __device__ uint32_t next_unvisited(int) const {
+        if (!__ballot_sync(FULL, mn_slot != EMPTY)) return EMPTY;
+        const uint32_t m1 = __reduce_min_sync(FULL, mn_slot == EMPTY ? 0xffffffffu : mn_key);
+        const bool c1 = mn_slot != EMPTY && mn_key == m1;
+        const uint32_t m2 = __reduce_min_sync(FULL, c1 ? mn_id : 0xffffffffu);
+        return __reduce_min_sync(FULL, (c1 && mn_id == m2) ? mn_slot : EMPTY);
     }
     __device__ void entry(uint32_t slot, uint32_t& id, float& sq, uint32_t& deg) const {
         id = W.id[slot];
@@ -534,12 +586,26 @@ struct TfbMem {
         __syncwarp();
         if (lane == 0) W.aux[slot] = a | VISITED;
         __syncwarp();
+        rescan(slot / S, lane);
     }
     __device__ void append(uint32_t id, float sq, uint32_t deg, int lane) {
+        const uint32_t slot = wsize;
         if (lane == 0) {
-            W.id[wsize] = id;
-            W.sq[wsize] = sq;
-            W.aux[wsize] = deg;
+            W.id[slot] = id;
+            W.sq[slot] = sq;
+            W.aux[slot] = deg;
+        }
+        if (static_cast<uint32_t>(lane) == slot / S) {  // the owner folds the new slot in
+            const uint32_t k = fkey(sq);
+            if (mn_slot == EMPTY || k < mn_key || (k == mn_key && id < mn_id)) {
+                mn_key = k;
+                mn_id = id;
+                mn_slot = slot;
+            }
+            if (mx_slot == EMPTY || k > mx_key) {
+                mx_key = k;
+                mx_slot = slot;
+            }
         }
         ++wsize;
         if (sq > zmax_sq || wsize == 1) {
@@ -582,7 +648,8 @@ struct TfbMem {
             W.aux[z] = deg;
         }
         __syncwarp();
-        recompute_zmax(lane);
+        rescan(z / S, lane);
+        zmax_from_caches();
     }
     __device__ void flush(Common& c, int lane) {
         for (uint32_t i = lane; i < wsize; i += 32) rl_append(c, W.id[i], W.sq[i], true, i);
@@ -612,6 +679,7 @@ struct TfbMem {
         __syncwarp();
         if (nm == 0) {
             zmax_sq = zmax_dist = 0.0f;
+            clear_caches();
             return false;
         }
         const Arr srt = warp_sort(mi, c.mo, nm, lane);
@@ -1208,7 +1276,7 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
 
 template <class TFB, bool EXACT, int NCH, bool PES>
 #ifndef PAG_MIN_BLOCKS
-#define PAG_MIN_BLOCKS 4
+#define PAG_MIN_BLOCKS PAG_OCC
 #endif
 __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const __grid_constant__ SearchLaunch P) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -1458,20 +1526,29 @@ cudaError_t dispatch_tfb(const SearchLaunch& L, int grid, cudaStream_t stream, i
 
 }  // namespace
 
-#if PAG_PES
-// construction-search instantiations (this file compiled again with
-// -DPAG_PES=1, keeping the PES code out of the query kernels)
-cudaError_t dispatch_pes(const SearchLaunch& L, int grid, cudaStream_t stream, int* bps) {
+#define PAG_CAT2(a, b, c) dispatch_p##a##_o##b##c
+#define PAG_CAT(a, b) PAG_CAT2(a, b, )
+cudaError_t dispatch_p0_o4(const SearchLaunch& L, int grid, cudaStream_t stream, int* bps);
+cudaError_t dispatch_p1_o4(const SearchLaunch& L, int grid, cudaStream_t stream, int* bps);
+cudaError_t dispatch_p0_o6(const SearchLaunch& L, int grid, cudaStream_t stream, int* bps);
+cudaError_t dispatch_p1_o6(const SearchLaunch& L, int grid, cudaStream_t stream, int* bps);
+
+cudaError_t PAG_CAT(PAG_PES, PAG_OCC)(const SearchLaunch& L, int grid, cudaStream_t stream, int* bps) {
     return dispatch_tfb(L, grid, stream, bps);
 }
-#else
-cudaError_t dispatch_pes(const SearchLaunch& L, int grid, cudaStream_t stream, int* bps);
 
+#if PAG_PES == 0 && PAG_OCC == 4
 namespace {
 cudaError_t dispatch(const SearchLaunch& L, int grid, cudaStream_t stream, int* bps) {
-    return L.collect_pes ? dispatch_pes(L, grid, stream, bps) : dispatch_tfb(L, grid, stream, bps);
+    const bool occ6 = search_high_occupancy(L);
+    if (L.collect_pes) return occ6 ? dispatch_p1_o6(L, grid, stream, bps) : dispatch_p1_o4(L, grid, stream, bps);
+    return occ6 ? dispatch_p0_o6(L, grid, stream, bps) : dispatch_p0_o4(L, grid, stream, bps);
 }
 }  // namespace
+
+// efS > 200: the marks outgrow the on-chip visited table (SURVEY.md §8(a)
+// a4: 1.6k-20k marks per query) and the HBM bitmap lookups dominate
+bool search_high_occupancy(const SearchLaunch& L) { return L.efS > 200 && !std::getenv("PAG_GPU_OCC4"); }
 
 size_t search_kernel_smem(const SearchLaunch& L) {
     return static_cast<size_t>(L.warp_smem_bytes) * L.warps_per_block;
@@ -1497,6 +1574,6 @@ cudaError_t search_occupancy(const SearchLaunch& L, int* blocks_per_sm) { return
 cudaError_t launch_search(const SearchLaunch& L, int grid, cudaStream_t stream) {
     return dispatch(L, grid, stream, nullptr);
 }
-#endif  // PAG_PES
+#endif
 
 }  // namespace pagdev
