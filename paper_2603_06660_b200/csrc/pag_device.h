@@ -86,7 +86,11 @@ struct SearchLaunch {
     uint32_t off_rl, rl_in_smem, rl_cap;  // R_L append buffer (+ sort scratch)
     uint32_t off_merge, merge_in_smem;
     uint32_t warps_per_block;
-    uint32_t tune;  // experiment bits (PAG_GPU_TUNE): 1 admit-time adjacency prefetch, 2 next-node prefetch
+    // experiment bits (PAG_GPU_TUNE): 8 sequential marks (diagnostic), 64
+    // row-pair reference-order distances. (Adjacency prefetch at admission
+    // or of the predicted next node, bulk or per-lane, measured slower on
+    // cfg2/cfg3/cfg4 and was removed.)
+    uint32_t tune;
 };
 
 size_t search_kernel_smem(const SearchLaunch& L);

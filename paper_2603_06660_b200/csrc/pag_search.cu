@@ -154,6 +154,18 @@ __device__ __forceinline__ bool marked(const Common& c, uint32_t id) {
     return (c.gbm[id >> 5] >> (id & 31u)) & 1u;
 }
 
+// the smem part of marked(): open-addressing probe only
+__device__ __forceinline__ bool hash_has(const Common& c, uint32_t id) {
+    const uint32_t mask = (1u << c.hs_log2) - 1;
+    uint32_t h = hslot(id, c.hs_log2);
+    while (true) {
+        const uint32_t v = c.hs[h];
+        if (v == id) return true;
+        if (v == EMPTY) return false;
+        h = (h + 1) & mask;
+    }
+}
+
 // warp-uniform call; lane 0 writes
 __device__ __forceinline__ void mark(Common& c, uint32_t id, int lane) {
     if (c.hs_count < (1u << c.hs_log2) / 2) {
@@ -1088,32 +1100,6 @@ __device__ __forceinline__ float code_sum(const float* T, uint32_t L, const uint
     return sum;
 }
 
-__device__ __forceinline__ void prefetch_block(const IndexView& ix, uint32_t u, uint32_t deg) {
-    if (deg == 0) return;
-    const uint8_t* blk = ix.adj + static_cast<uint64_t>(u) * ix.block_bytes;
-    const uint32_t S = ix.slot_stride;
-    const uint32_t b4 = (4u * deg + 15u) & ~15u;
-    prefetch_l2_bulk(blk, b4);
-    prefetch_l2_bulk(blk + 4u * S, b4);
-    prefetch_l2_bulk(blk + 8u * S, b4);
-    prefetch_l2_bulk(blk + 12u * S, b4);
-    prefetch_l2_bulk(blk + 16u * S, 4u * ix.cwp * deg);
-}
-
-// warp-parallel variant: lane i prefetches one 128-B line of the used part of
-// the block (4 scalar arrays, then the codes), one instruction for the warp
-__device__ __forceinline__ void prefetch_block_lanes(const IndexView& ix, uint32_t u, uint32_t deg, int lane) {
-    const uint8_t* blk = ix.adj + static_cast<uint64_t>(u) * ix.block_bytes;
-    const uint32_t S = ix.slot_stride;
-    const uint32_t lines_scalar = (4u * deg + 127u) / 128u;            // per scalar array
-    const uint32_t lines_codes = (4u * ix.cwp * deg + 127u) / 128u;
-    const uint32_t li = static_cast<uint32_t>(lane);
-    const uint8_t* p = nullptr;
-    if (li < 4u * lines_scalar) p = blk + (li / lines_scalar) * 4u * S + (li % lines_scalar) * 128u;
-    else if (li < 4u * lines_scalar + lines_codes) p = blk + 16u * S + (li - 4u * lines_scalar) * 128u;
-    if (p && deg) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
 // routing.cpp:139-204 for W slot `slot`; returns out.pes_rejected
 // (always false unless PES: the construction search with collect_pes)
 template <class TFB, bool EXACT, int NCH, bool PES>
@@ -1124,15 +1110,6 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
     float usq;
     s.entry(slot, u, usq, deg);
     s.set_visited(slot, lane);
-    // speculative L2 prefetch of the node expanded next if nothing nearer is
-    // admitted meanwhile (adjacency is the head of the next dependency chain)
-    {
-        const uint32_t nx = (P.tune & 2u) ? s.next_unvisited(lane) : EMPTY;
-        if (nx != EMPTY) {
-            const uint32_t nid = s.entry_id(nx), ndeg = s.entry_deg(nx);
-            if (lane == 0) prefetch_block(ix, nid, ndeg);
-        }
-    }
     ++c.n_visited;
     c.n_edges += deg;
     const float duq = __fsqrt_rn(usq);
@@ -1173,7 +1150,32 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
             }
         }
         PT(2);
-        const bool cand = active && !marked(c, w);
+        // visited (routing.hpp:104-105): the HBM bitmap word is requested
+        // before the smem probe and the PRT so that its latency overlaps them
+        uint32_t bmw = 0;
+        if (active && c.gt_used) bmw = __ldcg(c.gbm + (w >> 5));
+        const bool in_hs = active && hash_has(c, w);
+        // (i) speculative PRT at the group-start radius (evaluated for every
+        // active lane; only unmarked ones count)
+        const float adist0 = s.admission_dist();
+        float quot = 0.0f, tau0 = 0.0f;
+        bool pass0 = false, have_quot = false;
+        if (active) {
+            if (exact_mode) {
+                pass0 = true;
+            } else {
+                const float tau = prt_threshold(en, duq, adist0);
+                tau0 = tau;
+                if (tau < TAU_HI) {
+                    const uint32_t* cp = cw_a + static_cast<uint64_t>(j) * ix.cwp;
+                    const float sum = code_sum(c.T, ix.L, cp, ix.cwp, cw);
+                    quot = __fdiv_rn(__fdiv_rn(__fsub_rn(sum, bo), duq), cbeta);
+                    have_quot = true;
+                    pass0 = (tau <= -1.0f) || (quot >= tau);
+                }
+            }
+        }
+        const bool cand = active && !in_hs && !((bmw >> (w & 31u)) & 1u);
         PT(3);
         const uint32_t cand_mask = __ballot_sync(FULL, cand);
         // duplicate targets inside the group (reference order: a later copy
@@ -1183,25 +1185,7 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
         const uint32_t same = __match_any_sync(FULL, key) & cand_mask;
         const bool any_dup = __any_sync(FULL, __popc(same) > 1);
 
-        // (i) speculative PRT at the group-start radius
-        const float adist0 = s.admission_dist();
-        float quot = 0.0f, tau0 = 0.0f;
-        bool spec = false, have_quot = false;
-        if (cand) {
-            if (exact_mode) {
-                spec = true;
-            } else {
-                const float tau = prt_threshold(en, duq, adist0);
-                tau0 = tau;
-                if (tau < TAU_HI) {
-                    const uint32_t* cp = cw_a + static_cast<uint64_t>(j) * ix.cwp;
-                    const float sum = code_sum(c.T, ix.L, cp, ix.cwp, cw);
-                    quot = __fdiv_rn(__fdiv_rn(__fsub_rn(sum, bo), duq), cbeta);
-                    have_quot = true;
-                    spec = (tau <= -1.0f) || (quot >= tau);
-                }
-            }
-        }
+        const bool spec = cand && pass0;
         if (track_pes) {  // every edge, marked or not; quot does not depend on the radius
             float x = -CUDART_INF_F;
             if (active) {
@@ -1215,6 +1199,9 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
         }
         // (ii) compaction, (iii) exact distances of survivors
         const uint32_t surv = __ballot_sync(FULL, spec);
+#ifdef PAG_PHASE_TIMING
+        c.gt_count += __popc(surv) << 16;  // diagnostic: speculative survivors (high half of stat 7)
+#endif
         PT(4);
         if (surv) distances<EXACT, NCH>(P, c, surv, w, lane);
         PT(5);
@@ -1254,10 +1241,6 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
             if (P.tune & 8u) mark(c, w_j, lane);  // (diagnostic) sequential marking
             if (sq_j < s.admission_sq()) {
                 s.admit(w_j, sq_j, deg_j, lane);
-                // an admitted node is usually expanded later: start its
-                // adjacency on the way to L2 now (hides the next dependency)
-                if ((P.tune & 1u) && lane == 0) prefetch_block(ix, w_j, deg_j);
-                if (P.tune & 16u) prefetch_block_lanes(ix, w_j, deg_j, lane);
             } else {
                 s.push_fp(w_j, sq_j, deg_j, lane);
             }

@@ -28,10 +28,24 @@ ix.search_batch(q, params)
 fn(buf, 1)
 r = ix.search_batch(q, params)
 fn(buf, 1)
+buf = list(buf)
 names = ["setup+T+seeds", "-", "argmin/entry/adj-issue", "adjacency wait+visited", "PRT+codes",
          "distances", "replay", "end_round/flush/out"]
 tot = sum(buf)
 exp = r.stats[:, 3].sum()
+import torch  # noqa: E402
+nq = q.shape[0]
+qd = torch.from_numpy(q).cuda()
+outs = [torch.empty((nq, cfg["K"]), dtype=torch.int32, device="cuda"),
+        torch.empty((nq, cfg["K"]), dtype=torch.float32, device="cuda"),
+        torch.empty((nq,), dtype=torch.int32, device="cuda"), torch.empty((nq, 8), dtype=torch.int32, device="cuda")]
+ix.search_device(qd.data_ptr(), nq, params, *(t.data_ptr() for t in outs), 0)
+torch.cuda.synchronize()
+fn((C.c_ulonglong * 8)(), 1)  # (phase counters of this extra run are discarded)
+raw = outs[3].cpu().numpy().view(np.uint32)
+spec = float((raw[:, 7] >> 16).sum())
+print(f"speculative survivors {spec / nq:.1f} per query vs exact distances (passes + seeds) "
+      f"{r.stats[:, 0].mean():.1f}: {spec / r.stats[:, 2].sum():.3f} rows per pass")
 print(f"{cfg_name} efS={efs} exact={exact}: total warp-cycles {tot:.3e}; per expansion {tot / exp:.0f} cycles")
 for k in range(8):
     if buf[k]:
