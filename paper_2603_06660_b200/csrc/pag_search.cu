@@ -1366,22 +1366,41 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
 
         // ---- projection table (projection.cpp:123-137), serial dot per entry
         {
+            // four entries per lane at a time: four independent serial chains
+            // interleave instead of one chain's latency per entry
             const uint32_t Lm = ix.L * ix.m, sub = ix.sub_dim, m = ix.m;
-            for (uint32_t e = lane; e < Lm; e += 32) {
-                const uint32_t l = e / m, jj = e - l * m;
-                const float* xl = c.q + l * sub;
-                const float* rT = ix.refsT + static_cast<uint64_t>(l) * sub * m + jj;
-                float dot = 0.0f;
-                uint32_t cc = 0;
-                for (; cc + 8 <= sub; cc += 8) {  // 8 independent loads in flight, serial sum
-                    float rv[8];
+            for (uint32_t e0 = 0; e0 < Lm; e0 += 128) {
+                const float* xl[4];
+                const float* rT[4];
+                uint32_t to[4];
+                float dot[4];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) rv[i] = __ldg(rT + (cc + i) * m);
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) dot = __fadd_rn(dot, __fmul_rn(xl[cc + i], rv[i]));
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t e = min(e0 + lane + 32u * k, Lm - 1u);  // clamped lanes recompute a valid entry
+                    const uint32_t l = e / m, jj = e - l * m;
+                    xl[k] = c.q + l * sub;
+                    rT[k] = ix.refsT + static_cast<uint64_t>(l) * sub * m + jj;
+                    to[k] = l * 16 + jj;  // row stride 16 (m <= 16)
+                    dot[k] = 0.0f;
                 }
-                for (; cc < sub; ++cc) dot = __fadd_rn(dot, __fmul_rn(xl[cc], __ldg(rT + cc * m)));
-                c.T[l * 16 + jj] = dot;  // row stride 16 (m <= 16)
+                uint32_t cc = 0;
+                for (; cc + 4 <= sub; cc += 4) {
+                    float rv[4][4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) rv[k][i] = __ldg(rT[k] + (cc + i) * m);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) dot[k] = __fadd_rn(dot[k], __fmul_rn(xl[k][cc + i], rv[k][i]));
+                }
+                for (; cc < sub; ++cc)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) dot[k] = __fadd_rn(dot[k], __fmul_rn(xl[k][cc], __ldg(rT[k] + cc * m)));
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (e0 + lane + 32u * k < Lm) c.T[to[k]] = dot[k];
             }
         }
         __syncwarp();
