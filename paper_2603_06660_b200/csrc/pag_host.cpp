@@ -655,6 +655,26 @@ void run_search(pag_gpu_index& ix, Replica& r, const pag_search_params& p, const
     cuda_check(pagdev::launch_search(L, pl.grid, stream), "search kernel launch");
 }
 
+static_assert(sizeof(pag_search_stats) == 40, "pag_search_stats is five packed u64 (bindings rely on it)");
+
+// PAG_GPU_HOST_TRACE=1: per-call host phase times on stderr (diagnostic)
+struct HostTrace {
+    bool on = std::getenv("PAG_GPU_HOST_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    char buf[512];
+    int len = 0;
+    void mark(const char* what) {
+        if (!on) return;
+        const auto t = std::chrono::steady_clock::now();
+        len += std::snprintf(buf + len, sizeof(buf) - len, " %s %.1fus", what,
+                             std::chrono::duration<double, std::micro>(t - t0).count());
+        t0 = t;
+    }
+    ~HostTrace() {
+        if (on) std::fprintf(stderr, "[pag host]%s\n", buf);
+    }
+};
+
 // host-side construction request: nodes (host ids) and PES outputs
 struct ConstructionHost {
     const uint32_t* nodes;
@@ -668,6 +688,7 @@ void search_on_replica(pag_gpu_index& ix, Replica& r, const pag_search_params& p
                        pag_search_stats* stats, uint32_t* status_or, const ConstructionHost* ch = nullptr) {
     cuda_check(cudaSetDevice(r.device), "cudaSetDevice");
     if (nq == 0) return;
+    HostTrace tr;
     const uint32_t K = p.K;
     const size_t qb = ch ? 4ull * nq : 4ull * nq * ix.dim;
     const size_t ob_ids = 4ull * nq * std::max(1u, K), ob_n = 4ull * nq,
@@ -690,13 +711,39 @@ void search_on_replica(pag_gpu_index& ix, Replica& r, const pag_search_params& p
         ca.pes_n = reinterpret_cast<uint32_t*>(r.d_out + 2 * ob_ids + ob_n + ob_st + ob_list + ob_pes);
     }
     const ConstructionArgs* cap = ch ? &ca : nullptr;
-    cuda_check(cudaMemcpyAsync(r.d_q, ch ? static_cast<const void*>(ch->nodes) : static_cast<const void*>(q), qb,
-                               cudaMemcpyHostToDevice, r.stream),
-               "H2D queries");
-    run_search(ix, r, p, r.d_q, static_cast<uint32_t>(nq), nullptr, d_ids, d_sq, d_n, d_st, r.stream, 0, cap);
-    std::vector<uint32_t> st(nq * pagdev::kStatWords);
-    cuda_check(cudaMemcpyAsync(st.data(), d_st, ob_st, cudaMemcpyDeviceToHost, r.stream), "D2H stats");
+    // queries in pinned (mapped) host memory are read by the kernel in place
+    // over PCIe at each query's start (3 KB per query at d=768), which
+    // overlaps the transfer with the search; pageable ones are copied first
+    const float* q_src = r.d_q;
+    if (!ch) {
+        cudaPointerAttributes at{};
+        if (!std::getenv("PAG_GPU_NO_ZEROCOPY") && cudaPointerGetAttributes(&at, q) == cudaSuccess &&
+            at.type == cudaMemoryTypeHost && at.devicePointer)
+            q_src = static_cast<const float*>(at.devicePointer);
+        else
+            (void)cudaGetLastError();
+    }
+    if (q_src == r.d_q)
+        cuda_check(cudaMemcpyAsync(r.d_q, ch ? static_cast<const void*>(ch->nodes) : static_cast<const void*>(q), qb,
+                                   cudaMemcpyHostToDevice, r.stream),
+                   "H2D queries");
+    tr.mark("prep");
+    run_search(ix, r, p, q_src, static_cast<uint32_t>(nq), nullptr, d_ids, d_sq, d_n, d_st, r.stream, 0, cap);
+    tr.mark("launch");
+    // one D2H of the contiguous result block (ids | sq | n_out | counters)
+    // into pinned staging
+    const size_t ob_res = 2 * ob_ids + ob_n + ob_st;
+    if (r.h_pin_bytes < ob_res) {
+        if (r.h_pin) cudaFreeHost(r.h_pin);
+        r.h_pin = nullptr;
+        r.h_pin_bytes = 0;
+        cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&r.h_pin), ob_res, 0), "cudaHostAlloc");
+        r.h_pin_bytes = ob_res;
+    }
+    cuda_check(cudaMemcpyAsync(r.h_pin, r.d_out, ob_res, cudaMemcpyDeviceToHost, r.stream), "D2H results");
     cuda_check(cudaStreamSynchronize(r.stream), "search");
+    tr.mark("kernel+d2h");
+    const uint32_t* st = reinterpret_cast<const uint32_t*>(r.h_pin + 2 * ob_ids + ob_n);
     // visited-set overflow: re-run those queries with a 4x larger HBM table
     uint32_t grow = 2;
     for (int attempt = 0; attempt < 6; ++attempt) {
@@ -707,16 +754,16 @@ void search_on_replica(pag_gpu_index& ix, Replica& r, const pag_search_params& p
         if (redo.empty()) break;
         cuda_check(cudaMemcpyAsync(d_list, redo.data(), 4 * redo.size(), cudaMemcpyHostToDevice, r.stream),
                    "H2D retry list");
-        run_search(ix, r, p, r.d_q, static_cast<uint32_t>(redo.size()), d_list, d_ids, d_sq, d_n, d_st,
+        run_search(ix, r, p, q_src, static_cast<uint32_t>(redo.size()), d_list, d_ids, d_sq, d_n, d_st,
                    r.stream, grow, cap);
-        cuda_check(cudaMemcpyAsync(st.data(), d_st, ob_st, cudaMemcpyDeviceToHost, r.stream), "D2H stats");
+        cuda_check(cudaMemcpyAsync(r.h_pin, r.d_out, ob_res, cudaMemcpyDeviceToHost, r.stream), "D2H results");
         cuda_check(cudaStreamSynchronize(r.stream), "search retry");
     }
     if (K) {
-        cuda_check(cudaMemcpyAsync(ids, d_ids, 4ull * nq * K, cudaMemcpyDeviceToHost, r.stream), "D2H ids");
-        cuda_check(cudaMemcpyAsync(sq, d_sq, 4ull * nq * K, cudaMemcpyDeviceToHost, r.stream), "D2H sq");
+        std::memcpy(ids, r.h_pin, 4ull * nq * K);
+        std::memcpy(sq, r.h_pin + ob_ids, 4ull * nq * K);
     }
-    cuda_check(cudaMemcpyAsync(n_out, d_n, ob_n, cudaMemcpyDeviceToHost, r.stream), "D2H n_out");
+    std::memcpy(n_out, r.h_pin + 2 * ob_ids, ob_n);
     if (ch) {
         if (ob_pes) cuda_check(cudaMemcpyAsync(ch->pes, ca.pes, ob_pes, cudaMemcpyDeviceToHost, r.stream), "D2H pes");
         cuda_check(cudaMemcpyAsync(ch->pes_n, ca.pes_n, ob_pn, cudaMemcpyDeviceToHost, r.stream), "D2H pes_n");
@@ -738,6 +785,7 @@ void search_on_replica(pag_gpu_index& ix, Replica& r, const pag_search_params& p
         }
     }
     *status_or = so;
+    tr.mark("unpack");
 }
 
 // ---------------------------------------------------------------------------

@@ -147,16 +147,16 @@ class PagIndex:
             raise ValueError("query dimension mismatch")  # routing.cpp:252
         nq = q.shape[0]
         K = int(params.K)
-        ids = np.zeros((nq, K), np.uint32)
-        sq = np.zeros((nq, K), np.float32)
-        n_out = np.zeros(nq, np.uint32)
-        st = (SearchStatsC * max(nq, 1))()
+        # entries past n_out[i] are unspecified (as the device path)
+        ids = np.empty((nq, K), np.uint32)
+        sq = np.empty((nq, K), np.float32)
+        n_out = np.empty(nq, np.uint32)
+        stats = np.empty((nq, 5), np.uint64)  # pag_search_stats rows (5 x u64)
         pc = params.to_c()
         check(lib.pag_gpu_search(self._h, q.ctypes.data if nq else None, nq, C.byref(pc),
                                  ids.ctypes.data if K and nq else None,
                                  sq.ctypes.data if K and nq else None,
-                                 n_out.ctypes.data if nq else None, st))
-        stats = np.ctypeslib.as_array(C.cast(st, C.POINTER(C.c_uint64)), (max(nq, 1), 5))[:nq].copy()
+                                 n_out.ctypes.data if nq else None, stats.ctypes.data if nq else None))
         return BatchResult(ids, sq, n_out, stats)
 
     def construction_search(self, nodes, params: Optional[SearchParams] = None,
