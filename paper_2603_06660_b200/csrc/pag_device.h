@@ -71,7 +71,12 @@ struct SearchLaunch {
     uint32_t* out_pes;
     uint32_t* out_pes_n;
     // scheduling + scratch
+    // query claim counter of this launch, and the previous launch's, which
+    // this one zeroes once that launch has completed (programmatic dependent
+    // launch: consecutive launches alternate between two counters and two
+    // scratch sets, so a launch can start while its predecessor drains)
     uint32_t* qcounter;
+    uint32_t* qcounter_other;
     uint32_t* gbm;          // per slot: visited bitmap of gbm_words (all zero between queries)
     uint32_t gbm_words;     // multiple of 4 (>= n / 32)
     uint8_t* gscratch;      // per slot: gscratch_stride bytes

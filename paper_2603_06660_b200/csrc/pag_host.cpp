@@ -171,7 +171,8 @@ struct Replica {
     size_t slots = 0;
     uint8_t* gscratch = nullptr;
     size_t gscratch_bytes = 0;
-    uint32_t* qcounter = nullptr;
+    uint32_t* qcounter = nullptr;  // two claim counters (launch parity)
+    uint64_t seq = 0;              // search launches so far (parity of counters and scratch)
     // batch I/O
     float* d_q = nullptr;
     size_t d_q_bytes = 0;
@@ -356,6 +357,7 @@ std::unique_ptr<pag_gpu_index> open_index(const char* path, uint32_t device_mask
         dev_alloc(&r.refsT, 4ull * ix->refs.size());
         dev_alloc(&r.entries, 4ull * std::max<size_t>(1, n_entries));
         dev_alloc(&r.qcounter, 16);
+        cuda_check(cudaMemset(r.qcounter, 0, 16), "memset");
         r.bytes = n * row_bytes + 4ull * n + static_cast<size_t>(n) * ix->block_bytes +
                   4ull * ix->refs.size();
         r.cap_nodes = n;
@@ -500,7 +502,11 @@ struct Plan {
     int grid = 0;
 };
 
-constexpr int kWarpsPerBlock = 4;
+// warps (queries in flight) per CTA; PAG_GPU_WPB overrides (experiments)
+int warps_per_block() {
+    static const int w = std::getenv("PAG_GPU_WPB") ? std::max(1, std::min(4, std::atoi(std::getenv("PAG_GPU_WPB")))) : 4;
+    return w;
+}
 #ifndef PAG_WARP_SMEM_BUDGET
 #define PAG_WARP_SMEM_BUDGET (14 * 1024)
 #endif
@@ -521,6 +527,7 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     L.exact_dist = p.exact_dist;
     L.nq = nq;
     L.ix = ix.view(r);
+    const int kWarpsPerBlock = warps_per_block();
     L.warps_per_block = kWarpsPerBlock;
     L.tune = std::getenv("PAG_GPU_TUNE") ? static_cast<uint32_t>(std::atoi(std::getenv("PAG_GPU_TUNE"))) : 0u;
     L.stage_rows = 4;
@@ -597,22 +604,25 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
 
 void ensure_scratch(Replica& r, Plan& pl) {
     auto& L = pl.L;
-    const size_t slots = static_cast<size_t>(pl.grid) * kWarpsPerBlock;
+    const size_t slots = static_cast<size_t>(pl.grid) * pl.L.warps_per_block;
+    // two scratch sets (launch parity): a launch may overlap its predecessor
     if (slots > r.slots || L.gbm_words > r.gbm_words) {
         const size_t ns = std::max(slots, r.slots);
         const uint32_t words = std::max(L.gbm_words, r.gbm_words);
-        dev_free(r.gbm);
+        dev_free(r.gbm);  // (cudaFree waits for running kernels)
         r.gbm = nullptr;
-        dev_alloc(&r.gbm, ns * words * 4ull);
-        cuda_check(cudaMemset(r.gbm, 0, ns * words * 4ull), "memset");  // blocking: any stream may follow
+        dev_alloc(&r.gbm, 2 * ns * words * 4ull);
+        cuda_check(cudaMemset(r.gbm, 0, 2 * ns * words * 4ull), "memset");  // blocking: any stream may follow
         r.slots = ns;
         r.gbm_words = words;
     }
     L.gbm_words = r.gbm_words;
-    grow_dev(reinterpret_cast<void**>(&r.gscratch), &r.gscratch_bytes, r.slots * pl.gscratch_stride);
-    L.gbm = r.gbm;
-    L.gscratch = r.gscratch;
-    L.qcounter = r.qcounter;
+    grow_dev(reinterpret_cast<void**>(&r.gscratch), &r.gscratch_bytes, 2 * r.slots * pl.gscratch_stride);
+    const uint32_t par = static_cast<uint32_t>(r.seq & 1u);
+    L.gbm = r.gbm + par * r.slots * r.gbm_words;
+    L.gscratch = r.gscratch + par * r.slots * pl.gscratch_stride;
+    L.qcounter = r.qcounter + par;
+    L.qcounter_other = r.qcounter + (par ^ 1u);
 }
 
 void validate_params(const pag_gpu_index& ix, const pag_search_params& p) {
@@ -651,8 +661,8 @@ void run_search(pag_gpu_index& ix, Replica& r, const pag_search_params& p, const
     L.out_sq = sq;
     L.out_n = n_out;
     L.out_stats = stats;
-    cuda_check(cudaMemsetAsync(r.qcounter, 0, 4, stream), "memset");
     cuda_check(pagdev::launch_search(L, pl.grid, stream), "search kernel launch");
+    ++r.seq;
 }
 
 static_assert(sizeof(pag_search_stats) == 40, "pag_search_stats is five packed u64 (bindings rely on it)");

@@ -1295,12 +1295,33 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
     c.gbm_words = P.gbm_words;
     TFB s;
     s.init(P.b, sw, gw, P);
+    // Programmatic dependent launch (pag_host.cpp launch_t): this grid may
+    // start while the previous search launch on the stream drains its last
+    // queries. Everything before a warp's first output write only reads the
+    // index and this launch's own counter/scratch set; before that write the
+    // warp waits for the predecessor to complete, zeroes the predecessor's
+    // counter (the next launch's), and lets the next launch be scheduled.
+    bool released = false;
+    auto release = [&]() {
+        if (released) return;
+        released = true;
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (blockIdx.x == 0 && lane == 0) {
+            *P.qcounter_other = 0u;
+            __threadfence();
+        }
+        __syncwarp();
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    };
 
     while (true) {
         uint32_t qi = 0;
         if (lane == 0) qi = atomicAdd(P.qcounter, 1u);
         qi = __shfl_sync(FULL, qi, 0);
-        if (qi >= P.nq) break;
+        if (qi >= P.nq) {
+            release();
+            break;
+        }
         const uint32_t qid = P.qlist ? P.qlist[qi] : qi;
 
         // ---- reset (routing.cpp:12-30)
@@ -1335,6 +1356,7 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
             __syncwarp();
         }
         if (status) {
+            release();
             if (lane == 0) {
                 P.out_n[qid] = 0;
                 uint32_t* st = P.out_stats + static_cast<uint64_t>(qid) * kStatWords;
@@ -1449,6 +1471,7 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
                 if (i == EMPTY) break;
                 const uint32_t u = PES ? s.entry_id(i) : 0u;
                 if (expand<TFB, EXACT, NCH, PES>(P, c, s, i, lane)) {  // routing.cpp:235
+                    release();
                     if (lane == 0 && c.n_pes < P.pes_cap)
                         P.out_pes[static_cast<uint64_t>(qid) * P.pes_cap + c.n_pes] = u;
                     ++c.n_pes;
@@ -1467,6 +1490,7 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
         for (uint32_t i = lane; i < c.rl_size; i += 32) c.rl.aux[i] = 0u;
         __syncwarp();
         const Arr res = warp_sort(c.rl, c.rl_tmp, c.rl_size, lane);
+        release();
         for (uint32_t i = lane; i < k_out; i += 32) {
             P.out_ids[static_cast<uint64_t>(qid) * P.K + i] = res.id[i];
             P.out_sq[static_cast<uint64_t>(qid) * P.K + i] = res.sq[i];
@@ -1500,8 +1524,20 @@ cudaError_t launch_t(const SearchLaunch& L, int grid, size_t smem, cudaStream_t 
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     if (bps) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k, L.warps_per_block * 32, smem);
-    k<<<grid, L.warps_per_block * 32, smem, stream>>>(L);
-    return cudaGetLastError();
+    // programmatic stream serialisation: the grid may be scheduled once the
+    // previous search grid on the stream has triggered (see release())
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(L.warps_per_block * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    static const int pdl = std::getenv("PAG_GPU_NO_PDL") ? 0 : 1;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, L);
 }
 
 template <class TFB, bool EXACT>
