@@ -285,3 +285,44 @@ def test_construction_device_path_matches_host_path(pag, built):
     for i in range(nn):  # entries past pes_n are unspecified on the device path
         m = min(int(host.pes_n[i]), cap)
         assert np.array_equal(pes[i, :m], host.pes[i, :m])
+
+
+def test_back_to_back_launches_keep_stream_order(pag, built):
+    """Consecutive launches overlap (programmatic dependent launch): a batch
+    written into the same output buffers right after another must still end
+    with the later batch's results, across alternating counter/scratch sets
+    and changing batch sizes."""
+    import torch
+    fx = built("deg64")
+    ix = gpu_index(pag, fx["index"])
+    p = pag.SearchParams(K=10, efS=60)
+    qa = fx["queries"]
+    qb = np.ascontiguousarray(qa[::-1] * 1.01, np.float32)
+    want_a = ix.search_batch(qa, p)
+    want_b = ix.search_batch(qb, p)
+    nq = qa.shape[0]
+    s = torch.cuda.Stream()
+    da, db = torch.from_numpy(qa).cuda(), torch.from_numpy(qb).cuda()
+    ids = torch.zeros((nq, 10), dtype=torch.int32, device="cuda")
+    sq = torch.zeros((nq, 10), dtype=torch.float32, device="cuda")
+    n = torch.zeros((nq,), dtype=torch.int32, device="cuda")
+    st = torch.zeros((nq, 8), dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    for rep in range(7):
+        src, want, m = ((da, want_a, nq) if rep % 2 == 0 else (db, want_b, nq - 3 * rep))
+        ix.search_device(src.data_ptr(), m, p, ids.data_ptr(), sq.data_ptr(), n.data_ptr(), st.data_ptr(),
+                         s.cuda_stream)
+    s.synchronize()
+    # the last launch (rep 6, batch A, all queries) wins everywhere
+    assert np.array_equal(ids.cpu().numpy().view(np.uint32), want_a.ids)
+    assert np.array_equal(sq.cpu().numpy(), want_a.sq)
+    assert np.array_equal(st.cpu().numpy()[:, :5].astype(np.uint64), want_a.stats)
+    for rep in range(3):  # B after A: B's rows win, rows past B's count keep A's
+        ix.search_device(da.data_ptr(), nq, p, ids.data_ptr(), sq.data_ptr(), n.data_ptr(), st.data_ptr(),
+                         s.cuda_stream)
+        ix.search_device(db.data_ptr(), nq - 5, p, ids.data_ptr(), sq.data_ptr(), n.data_ptr(), st.data_ptr(),
+                         s.cuda_stream)
+    s.synchronize()
+    got = ids.cpu().numpy().view(np.uint32)
+    assert np.array_equal(got[:nq - 5], want_b.ids[:nq - 5])
+    assert np.array_equal(got[nq - 5:], want_a.ids[nq - 5:])
