@@ -83,6 +83,7 @@ __device__ __forceinline__ float prt_threshold(float en, float duq, float dz) {
     return __fdiv_rn(num, den);
 }
 
+
 __device__ __forceinline__ uint32_t hslot(uint32_t id, uint32_t log2) {
     return (id * 2654435761u) >> (32 - log2);
 }
@@ -338,9 +339,9 @@ struct TfbReg {
         const bool v = static_cast<uint32_t>(lane) < wsize;
         const uint32_t k = v ? fkey(w_sq) : 0u;
         const uint32_t m = __reduce_max_sync(FULL, k);
-        zmax_idx = __ffs(__ballot_sync(FULL, v && k == m)) - 1;
-        zmax_sq = __shfl_sync(FULL, w_sq, zmax_idx);
+        zmax_sq = __uint_as_float(m);  // the key is the value (sq >= 0: x + 0 == x)
         zmax_dist = __fsqrt_rn(zmax_sq);
+        zmax_idx = __ffs(__ballot_sync(FULL, v && k == m)) - 1;
     }
     // routing.cpp:71-80: argmin over unvisited by (sq, id); `skip` excluded
     __device__ uint32_t next_unvisited(int lane, uint32_t skip = EMPTY) const {
@@ -563,9 +564,9 @@ struct TfbMem {
     // routing.cpp:32-44 from the caches: argmax, first slot on ties
     __device__ void zmax_from_caches() {
         const uint32_t m = __reduce_max_sync(FULL, mx_slot == EMPTY ? 0u : mx_key);
-        zmax_idx = __reduce_min_sync(FULL, (mx_slot != EMPTY && mx_key == m) ? mx_slot : EMPTY);
-        zmax_sq = W.sq[zmax_idx];
+        zmax_sq = __uint_as_float(m);  // the key is the value (sq >= 0: x + 0 == x)
         zmax_dist = __fsqrt_rn(zmax_sq);
+        zmax_idx = __reduce_min_sync(FULL, (mx_slot != EMPTY && mx_key == m) ? mx_slot : EMPTY);
     }
     __device__ void recompute_zmax(int lane) {  // after a wholesale refill of W
         clear_caches();
