@@ -461,8 +461,27 @@ def run_pag(args, cfg, paths, rank, world, local_rank, threads, dist):
     t = time.perf_counter()
     for _ in range(e2e_steps):
         ix.search_batch(qh, params)
-    e2e_s = max(time.perf_counter() - t, 1e-9)
-    e2e_s = max_over_ranks(e2e_s, dist, dev)
+    sync_s = max_over_ranks(max(time.perf_counter() - t, 1e-9), dist, dev)
+    # the same through the asynchronous API, up to 3 batches in flight: the
+    # kernel reads each step's pinned queries in place and writes its results
+    # into pinned host memory; wait() unpacks them into the step's arrays
+    if dist is not None:
+        dist.barrier()
+    outs = [pag.BatchResult(np.zeros((nq, K), np.uint32), np.zeros((nq, K), np.float32), np.zeros(nq, np.uint32),
+                            np.zeros((nq, 5), np.uint64)) for _ in range(4)]  # rotating result buffers
+    for i in range(4 if e2e_steps else 0):  # warm-up: pinned slot buffers, first touch of the arrays
+        ix.search_submit(qh, params, out=outs[i]).wait()
+    if dist is not None:
+        dist.barrier()
+    t = time.perf_counter()
+    pending = []
+    for i in range(e2e_steps):
+        pending.append(ix.search_submit(qh, params, out=outs[i % 4]))
+        if len(pending) == 3:
+            pending.pop(0).wait()
+    while pending:
+        pending.pop(0).wait()
+    e2e_s = max_over_ranks(max(time.perf_counter() - t, 1e-9), dist, dev)
     e2e_qps = world * nq * e2e_steps / e2e_s
     h2d = nq * queries.shape[1] * 4
     d2h = nq * K * 8 + nq * 4 + nq * 8 * 4
@@ -512,7 +531,12 @@ def run_pag(args, cfg, paths, rank, world, local_rank, threads, dist):
                                "written only after the previous launch completes); events around all K",
                    "parallelism": f"query shards, index replica per GPU x{world}"},
         "e2e": {"value": round(e2e_qps, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
+                "d2h_bytes_per_step": d2h,
+                "path": "pag_gpu_search_submit/wait from pinned host queries, up to 3 batches in flight "
+                        "(queries read in place over PCIe, results written to pinned host memory, "
+                        "unpacked into 4 rotating preallocated result arrays)",
+                "sync_value": round(world * nq * e2e_steps / sync_s, 1),
+                "sync_path": "pag_gpu_search, one blocking call per step"},
         "gpu_launches": args.steps,  # one pag_search_kernel launch per step
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,

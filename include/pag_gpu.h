@@ -105,6 +105,19 @@ int pag_gpu_search_device(pag_gpu_index* ix, const float* q_dev, uint64_t nq,
                           const pag_search_params* params, uint32_t* ids_dev, float* sq_dev,
                           uint32_t* n_out_dev, uint32_t* stats_dev, void* stream);
 
+/* Asynchronous pag_gpu_search: enqueues the batch and returns a ticket; the
+ * results land in the caller's ids / sq / n_out / stats when
+ * pag_gpu_search_wait(ticket) returns (host buffers must stay valid until
+ * then). Queries in pinned host memory are read by the kernel in place;
+ * pageable ones are copied at submit. Up to 4 batches are in flight per GPU
+ * (a 5th submit first completes the oldest); consecutive batches overlap on
+ * the GPU like back-to-back pag_gpu_search_device calls. Errors of a batch
+ * (e.g. "zero query under cosine metric") are reported by the call that
+ * completes it. Calls on one handle serialise. */
+int pag_gpu_search_submit(pag_gpu_index* ix, const float* q, uint64_t nq, const pag_search_params* params,
+                          uint32_t* ids, float* sq, uint32_t* n_out, pag_search_stats* stats, uint64_t* ticket);
+int pag_gpu_search_wait(pag_gpu_index* ix, uint64_t ticket);
+
 /* Construction search. Replaces the search step of
  *   insert_with_state(PagIndex&, uint32_t v, PesSet&, TfbState&)
  *   proj/src/builder.cpp:218-227 — search_padded(index, vectors().row(v), sp)

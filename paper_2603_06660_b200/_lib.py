@@ -29,6 +29,8 @@ EXPORTS = (
     "pag_gpu_info",
     "pag_gpu_search",
     "pag_gpu_search_device",
+    "pag_gpu_search_submit",
+    "pag_gpu_search_wait",
     "pag_gpu_construction_search",
     "pag_gpu_construction_search_device",
     "pag_gpu_ground_truth",
@@ -73,6 +75,10 @@ def _load():
         "pag_gpu_search_device": (C.c_int, [P, C.c_void_p, C.c_uint64, C.POINTER(SearchParamsC),
                                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                             C.c_void_p]),
+        "pag_gpu_search_submit": (C.c_int, [P, C.c_void_p, C.c_uint64, C.POINTER(SearchParamsC),
+                                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                            C.POINTER(C.c_uint64)]),
+        "pag_gpu_search_wait": (C.c_int, [P, C.c_uint64]),
         "pag_gpu_construction_search": (C.c_int, [P, C.c_void_p, C.c_uint64, C.c_void_p, C.c_int,
                                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                                   C.c_void_p, C.c_uint32, C.c_void_p]),

@@ -77,6 +77,13 @@ struct SearchLaunch {
     // scratch sets, so a launch can start while its predecessor drains)
     uint32_t* qcounter;
     uint32_t* qcounter_other;
+    // asynchronous host API (pag_gpu_search_submit): when host_flag is set,
+    // the last warp to exit writes flag_value to this pinned host word after
+    // a system-scope fence (all outputs, written to pinned host memory, are
+    // then visible); done_ctr counts exited warps (n_warps in the grid)
+    uint32_t* done_ctr;
+    uint32_t* host_flag;
+    uint32_t flag_value, n_warps;
     uint32_t* gbm;          // per slot: visited bitmap of gbm_words (all zero between queries)
     uint32_t gbm_words;     // multiple of 4 (>= n / 32)
     uint8_t* gscratch;      // per slot: gscratch_stride bytes

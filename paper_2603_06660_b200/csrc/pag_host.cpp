@@ -15,6 +15,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -180,6 +181,25 @@ struct Replica {
     size_t d_out_bytes = 0;
     uint8_t* h_pin = nullptr;
     size_t h_pin_bytes = 0;
+    // asynchronous batches (pag_gpu_search_submit): a ring of in-flight
+    // requests whose kernels write results straight into pinned host memory
+    struct AsyncSlot {
+        uint8_t* h_res = nullptr;  // pinned, mapped: ids | sq | n_out | counters
+        size_t h_bytes = 0;
+        float* d_q = nullptr;      // device copy of pageable queries
+        size_t d_q_bytes = 0;
+        uint64_t ticket = 0;       // 0 = free
+        uint64_t nq = 0;
+        uint32_t K = 0;
+        uint32_t* ids = nullptr;
+        float* sq = nullptr;
+        uint32_t* n_out = nullptr;
+        pag_search_stats* stats = nullptr;
+    };
+    static constexpr int kAsyncDepth = 4;
+    AsyncSlot aslot[kAsyncDepth];
+    uint32_t* h_flags = nullptr;  // pinned, mapped: one completion word per slot
+    uint32_t* d_done = nullptr;   // device: exited-warp counters per slot
 };
 
 template <typename T>
@@ -203,6 +223,7 @@ void grow_dev(void** p, size_t* cap, size_t need) {
 }  // namespace
 
 struct pag_gpu_index {
+    uint64_t async_seq = 0;  // tickets issued by pag_gpu_search_submit
     uint64_t n = 0;
     uint32_t dim = 0, padded = 0, dstride = 0, L = 0, m = 0, M = 0, efC = 0, b_build = 0,
              pes_flush = 0;
@@ -254,6 +275,13 @@ void free_replica(Replica& r) {
                     static_cast<void*>(r.d_q), static_cast<void*>(r.d_out), static_cast<void*>(r.bnorm)})
         dev_free(p);
     if (r.h_pin) cudaFreeHost(r.h_pin);
+    if (r.stream) cudaStreamSynchronize(r.stream);  // in-flight asynchronous batches
+    for (auto& a : r.aslot) {
+        if (a.h_res) cudaFreeHost(a.h_res);
+        dev_free(a.d_q);
+    }
+    if (r.h_flags) cudaFreeHost(r.h_flags);
+    dev_free(r.d_done);
     if (r.stream) cudaStreamDestroy(r.stream);
     r = Replica{};
 }
@@ -630,6 +658,13 @@ void validate_params(const pag_gpu_index& ix, const pag_search_params& p) {
     if (p.K > p.efS) throw_err(PAG_GPU_EINVAL, "K > efS");                // routing.cpp:209
 }
 
+// asynchronous-batch completion signalling (see SearchLaunch::host_flag)
+struct AsyncArgs {
+    uint32_t* done_ctr = nullptr;
+    uint32_t* host_flag = nullptr;  // device address of the pinned word
+    uint32_t flag_value = 0;
+};
+
 // construction search (builder.cpp:218-227) device-side extras
 struct ConstructionArgs {
     const uint32_t* nodes = nullptr;  // device: query i = stored row of nodes[i]
@@ -643,11 +678,17 @@ struct ConstructionArgs {
 void run_search(pag_gpu_index& ix, Replica& r, const pag_search_params& p, const float* q_dev,
                 uint32_t nq, const uint32_t* qlist, uint32_t* ids, float* sq, uint32_t* n_out,
                 uint32_t* stats, cudaStream_t stream, uint32_t gt_log2_min,
-                const ConstructionArgs* ca = nullptr) {
+                const ConstructionArgs* ca = nullptr, const AsyncArgs* aa = nullptr) {
     if (nq == 0) return;
     Plan pl = make_plan(ix, r, p, nq, gt_log2_min);
     ensure_scratch(r, pl);
     auto& L = pl.L;
+    if (aa) {
+        L.done_ctr = aa->done_ctr;
+        L.host_flag = aa->host_flag;
+        L.flag_value = aa->flag_value;
+        L.n_warps = static_cast<uint32_t>(pl.grid) * L.warps_per_block;
+    }
     L.queries = q_dev;
     L.qlist = qlist;
     if (ca) {
@@ -1091,6 +1132,123 @@ int guarded(F&& f) {
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// Asynchronous batches: submit returns after the launch; the kernel reads
+// pinned queries in place, writes results into the slot's pinned block and
+// raises the slot's completion word; wait spins on that word and unpacks.
+// Consecutive submits keep the programmatic-dependent-launch overlap (no
+// event or copy between the kernels).
+// ---------------------------------------------------------------------------
+void async_complete(pag_gpu_index& ix, Replica& r, Replica::AsyncSlot& a, uint32_t* status_or) {
+    (void)ix;
+    const int si = static_cast<int>(&a - r.aslot);
+    volatile uint32_t* flag = r.h_flags + si;
+    const uint32_t want = static_cast<uint32_t>(a.ticket);
+    uint64_t spins = 0;
+    while (*flag != want) {
+        if ((++spins & 1023u) == 0) {
+            const cudaError_t e = cudaStreamQuery(r.stream);
+            if (e != cudaSuccess && e != cudaErrorNotReady) cuda_check(e, "asynchronous search");
+            if (e == cudaSuccess && *flag != want) {
+                a.ticket = 0;
+                throw_err(PAG_GPU_ECUDA, "asynchronous search: completion flag missing");
+            }
+            std::this_thread::yield();
+        }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    const uint64_t nq = a.nq;
+    const uint32_t K = a.K;
+    const size_t ob_ids = 4ull * nq * std::max(1u, K), ob_n = 4ull * nq;
+    if (K) {
+        std::memcpy(a.ids, a.h_res, 4ull * nq * K);
+        std::memcpy(a.sq, a.h_res + ob_ids, 4ull * nq * K);
+    }
+    std::memcpy(a.n_out, a.h_res + 2 * ob_ids, ob_n);
+    const uint32_t* st = reinterpret_cast<const uint32_t*>(a.h_res + 2 * ob_ids + ob_n);
+    uint32_t so = 0;
+    for (uint64_t i = 0; i < nq; ++i) {
+        const uint32_t* w = st + i * pagdev::kStatWords;
+        so |= w[pagdev::kStatStatus];
+        if (a.stats) {
+            a.stats[i].exact_dist_count = w[pagdev::kStatExact];
+            a.stats[i].test_count = w[pagdev::kStatTest];
+            a.stats[i].pass_count = w[pagdev::kStatPass];
+            a.stats[i].visited_count = w[pagdev::kStatVisited];
+            a.stats[i].edges_scanned = w[pagdev::kStatEdges];
+        }
+    }
+    a.ticket = 0;
+    *status_or |= so;
+}
+
+void async_submit_replica(pag_gpu_index& ix, Replica& r, const pag_search_params& p, const float* q,
+                          uint64_t nq, uint32_t* ids, float* sq, uint32_t* n_out, pag_search_stats* stats,
+                          uint64_t ticket, uint32_t* status_or) {
+    cuda_check(cudaSetDevice(r.device), "cudaSetDevice");
+    if (!r.h_flags) {
+        cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&r.h_flags), 4 * Replica::kAsyncDepth, cudaHostAllocMapped),
+                   "cudaHostAlloc");
+        std::memset(r.h_flags, 0, 4 * Replica::kAsyncDepth);
+        dev_alloc(&r.d_done, 4 * Replica::kAsyncDepth);
+        cuda_check(cudaMemset(r.d_done, 0, 4 * Replica::kAsyncDepth), "memset");
+    }
+    const int si = static_cast<int>(ticket % Replica::kAsyncDepth);
+    Replica::AsyncSlot& a = r.aslot[si];
+    if (a.ticket) async_complete(ix, r, a, status_or);  // ring full: finish the oldest first
+    if (nq == 0) return;
+    const uint32_t K = p.K;
+    const size_t ob_ids = 4ull * nq * std::max(1u, K), ob_n = 4ull * nq, ob_st = 4ull * nq * pagdev::kStatWords;
+    const size_t need = 2 * ob_ids + ob_n + ob_st;
+    if (a.h_bytes < need) {
+        if (a.h_res) cudaFreeHost(a.h_res);
+        a.h_res = nullptr;
+        a.h_bytes = 0;
+        cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&a.h_res), need, cudaHostAllocMapped), "cudaHostAlloc");
+        a.h_bytes = need;
+    }
+    uint8_t* dres = nullptr;
+    cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dres), a.h_res, 0), "cudaHostGetDevicePointer");
+    uint32_t* dflags = nullptr;
+    cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dflags), r.h_flags, 0), "cudaHostGetDevicePointer");
+    const float* q_src = nullptr;
+    cudaPointerAttributes at{};
+    if (!std::getenv("PAG_GPU_NO_ZEROCOPY") && cudaPointerGetAttributes(&at, q) == cudaSuccess &&
+        at.type == cudaMemoryTypeHost && at.devicePointer) {
+        q_src = static_cast<const float*>(at.devicePointer);
+    } else {
+        (void)cudaGetLastError();
+        grow_dev(reinterpret_cast<void**>(&a.d_q), &a.d_q_bytes, 4ull * nq * ix.dim);
+        cuda_check(cudaMemcpyAsync(a.d_q, q, 4ull * nq * ix.dim, cudaMemcpyHostToDevice, r.stream), "H2D queries");
+        q_src = a.d_q;
+    }
+    AsyncArgs aa;
+    aa.done_ctr = r.d_done + si;
+    aa.host_flag = dflags + si;
+    aa.flag_value = static_cast<uint32_t>(ticket);
+    r.h_flags[si] = 0;
+    a.ticket = ticket;
+    a.nq = nq;
+    a.K = K;
+    a.ids = ids;
+    a.sq = sq;
+    a.n_out = n_out;
+    a.stats = stats;
+    try {
+        run_search(ix, r, p, q_src, static_cast<uint32_t>(nq), nullptr, reinterpret_cast<uint32_t*>(dres),
+                   reinterpret_cast<float*>(dres + ob_ids), reinterpret_cast<uint32_t*>(dres + 2 * ob_ids),
+                   reinterpret_cast<uint32_t*>(dres + 2 * ob_ids + ob_n), r.stream, 0, nullptr, &aa);
+    } catch (...) {
+        a.ticket = 0;
+        throw;
+    }
+}
+
+void check_status(uint32_t so) {
+    if (so & pagdev::kStatusZeroCosineQuery) throw_err(PAG_GPU_EINVAL, "zero query under cosine metric");
+    if (so & pagdev::kStatusVisitedOverflow) throw_err(PAG_GPU_ERUNTIME, "visited set overflow after retries");
+}
+
 extern "C" {
 
 void pag_gpu_default_params(pag_search_params* p) {
@@ -1281,6 +1439,45 @@ int pag_gpu_construction_search_device(pag_gpu_index* ix, const uint32_t* nodes_
         ca.pes_n = pes_n_dev;
         run_search(*ix, r, p, nullptr, static_cast<uint32_t>(nn), nullptr, ids_dev, sq_dev, n_out_dev, stats_dev,
                    static_cast<cudaStream_t>(stream), 0, &ca);
+    });
+}
+
+int pag_gpu_search_submit(pag_gpu_index* ix, const float* q, uint64_t nq, const pag_search_params* params,
+                          uint32_t* ids, float* sq, uint32_t* n_out, pag_search_stats* stats, uint64_t* ticket) {
+    return guarded([&] {
+        if (!ix || !params || !ticket) throw_err(PAG_GPU_EINVAL, "null argument");
+        std::lock_guard<std::mutex> g(ix->mu);
+        const pag_search_params p = *params;
+        validate_params(*ix, p);
+        if (nq && (!q || !n_out || (p.K && (!ids || !sq)))) throw_err(PAG_GPU_EINVAL, "null argument");
+        if (nq >= 0xFFFFFFFFull) throw_err(PAG_GPU_EINVAL, "batch too large");
+        const uint64_t t = ++ix->async_seq;
+        *ticket = t;
+        const size_t nd = ix->reps.size();
+        uint32_t so = 0;
+        for (size_t d = 0; d < nd; ++d) {
+            const uint64_t q0 = nq * d / nd, q1 = nq * (d + 1) / nd;
+            async_submit_replica(*ix, ix->reps[d], p, q + q0 * ix->dim, q1 - q0, ids + q0 * p.K, sq + q0 * p.K,
+                                 n_out + q0, stats ? stats + q0 : nullptr, t, &so);
+        }
+        check_status(so);  // (from an older batch completed to free its slot)
+    });
+}
+
+int pag_gpu_search_wait(pag_gpu_index* ix, uint64_t ticket) {
+    return guarded([&] {
+        if (!ix) throw_err(PAG_GPU_EINVAL, "null argument");
+        std::lock_guard<std::mutex> g(ix->mu);
+        if (ticket == 0 || ticket > ix->async_seq) throw_err(PAG_GPU_EINVAL, "unknown ticket");
+        uint32_t so = 0;
+        for (auto& r : ix->reps) {
+            Replica::AsyncSlot& a = r.aslot[ticket % Replica::kAsyncDepth];
+            if (a.ticket == ticket) {
+                cuda_check(cudaSetDevice(r.device), "cudaSetDevice");
+                async_complete(*ix, r, a, &so);
+            }
+        }
+        check_status(so);
     });
 }
 

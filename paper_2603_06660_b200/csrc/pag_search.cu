@@ -1517,6 +1517,15 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
     if (lane == 0)
         for (int k = 0; k < 8; ++k) atomicAdd(&g_phase[k], static_cast<unsigned long long>(c.pt_acc[k]));
 #endif
+    if (P.host_flag) {  // grid-completion flag for the asynchronous host API
+        __threadfence_system();  // every lane's output writes (pinned host memory)
+        __syncwarp();
+        if (lane == 0 && atomicAdd(P.done_ctr, 1u) + 1u == P.n_warps) {
+            *P.done_ctr = 0u;  // ready for the slot's next launch
+            __threadfence_system();
+            *reinterpret_cast<volatile uint32_t*>(P.host_flag) = P.flag_value;
+        }
+    }
 }
 
 template <class TFB, bool EXACT, int NCH>

@@ -79,6 +79,22 @@ class BatchResult:
                             SearchStats(*(int(x) for x in s)))
 
 
+class PendingBatch:
+    """An in-flight asynchronous batch (pag_gpu_search_submit); keeps the
+    query and result arrays alive until wait()."""
+
+    def __init__(self, index: "PagIndex", ticket: int, queries: np.ndarray, result: BatchResult):
+        self._index, self.ticket, self._q, self._res = index, ticket, queries, result
+        self._done = False
+
+    def wait(self) -> BatchResult:
+        if not self._done:
+            check(lib.pag_gpu_search_wait(self._index.handle, self.ticket))
+            self._done = True
+            self._q = None
+        return self._res
+
+
 @dataclass
 class ConstructionResult(BatchResult):
     """BatchResult plus SearchResult.pes_rejected (routing.hpp:176) per node:
@@ -158,6 +174,38 @@ class PagIndex:
                                  sq.ctypes.data if K and nq else None,
                                  n_out.ctypes.data if nq else None, stats.ctypes.data if nq else None))
         return BatchResult(ids, sq, n_out, stats)
+
+    def search_submit(self, queries: np.ndarray, params: SearchParams,
+                      out: Optional[BatchResult] = None) -> "PendingBatch":
+        """Asynchronous search_batch: returns at once; PendingBatch.wait()
+        gives the BatchResult (written into `out` when given: reusing result
+        arrays avoids first-touch page faults). Pinned query arrays are read
+        in place by the kernel (keep them alive and unmodified until wait)."""
+        q = np.ascontiguousarray(queries, np.float32)
+        if q.ndim == 1:
+            q = q.reshape(1, -1)
+        if q.shape[1] != self.dim:
+            raise ValueError("query dimension mismatch")  # routing.cpp:252
+        nq = q.shape[0]
+        K = int(params.K)
+        if out is not None:
+            if (out.ids.shape != (nq, K) or out.sq.shape != (nq, K) or out.n_out.shape != (nq,)
+                    or out.stats.shape != (nq, 5) or out.ids.dtype != np.uint32 or out.sq.dtype != np.float32
+                    or out.n_out.dtype != np.uint32 or out.stats.dtype != np.uint64
+                    or not all(a.flags.c_contiguous for a in (out.ids, out.sq, out.n_out, out.stats))):
+                raise ValueError("out arrays do not match the batch")
+            res = out
+        else:
+            res = BatchResult(np.empty((nq, K), np.uint32), np.empty((nq, K), np.float32),
+                              np.empty(nq, np.uint32), np.empty((nq, 5), np.uint64))
+        t = C.c_uint64(0)
+        pc = params.to_c()
+        check(lib.pag_gpu_search_submit(self._h, q.ctypes.data if nq else None, nq, C.byref(pc),
+                                        res.ids.ctypes.data if K and nq else None,
+                                        res.sq.ctypes.data if K and nq else None,
+                                        res.n_out.ctypes.data if nq else None,
+                                        res.stats.ctypes.data if nq else None, C.byref(t)))
+        return PendingBatch(self, int(t.value), q, res)
 
     def construction_search(self, nodes, params: Optional[SearchParams] = None,
                             collect_pes: Optional[bool] = None, pes_cap: int = 256) -> ConstructionResult:

@@ -326,3 +326,27 @@ def test_back_to_back_launches_keep_stream_order(pag, built):
     got = ids.cpu().numpy().view(np.uint32)
     assert np.array_equal(got[:nq - 5], want_b.ids[:nq - 5])
     assert np.array_equal(got[nq - 5:], want_a.ids[nq - 5:])
+
+
+def test_async_submit_wait_matches_sync(pag, built):
+    """pag_gpu_search_submit / wait: results written by the kernel into pinned
+    host memory, several batches in flight (more than the ring depth), pinned
+    queries read in place and pageable ones copied."""
+    import torch
+    fx = built("euc48")
+    ix = gpu_index(pag, fx["index"])
+    p = pag.SearchParams(K=10, efS=50)
+    want = ix.search_batch(fx["queries"], p)
+    pinned = torch.empty(fx["queries"].shape, dtype=torch.float32, pin_memory=True)
+    pinned.numpy()[:] = fx["queries"]
+    pend = [ix.search_submit(pinned.numpy() if i % 2 else fx["queries"], p) for i in range(7)]
+    for pb in pend[::-1]:  # out of order; the first ones were completed to free ring slots
+        r = pb.wait()
+        assert_same_results((r.ids, r.sq, r.n_out, r.stats), (want.ids, want.sq, want.n_out, want.stats), "async")
+    with pytest.raises(ValueError, match="K > efS"):
+        ix.search_submit(fx["queries"], pag.SearchParams(K=20, efS=10))
+    cos = gpu_index(pag, built("cos20")["index"])
+    bad = np.zeros((3, 20), np.float32)
+    pb = cos.search_submit(bad, pag.SearchParams(K=5, efS=20))
+    with pytest.raises(ValueError, match="zero query under cosine metric"):
+        pb.wait()
