@@ -216,19 +216,6 @@ __device__ __forceinline__ void clear_bitmap(Common& c, int lane) {
     __syncwarp();
 }
 
-// number of entries of sorted a[0..n) strictly less than (v, id)
-__device__ __forceinline__ uint32_t count_less(const Arr& a, uint32_t n, float v, uint32_t id) {
-    uint32_t lo = 0, hi = n;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (cless(a.sq[mid], a.id[mid], v, id))
-            lo = mid + 1;
-        else
-            hi = mid;
-    }
-    return lo;
-}
-
 // routing.cpp:82-90: R_L receives flushed W entries (distinct ids); they are
 // appended and the capacity-limited sorted list is formed at the end.
 __device__ __forceinline__ void rl_append(Common& c, uint32_t id, float sq, bool valid, uint32_t offset) {
@@ -258,11 +245,43 @@ __device__ __forceinline__ void bitonic32(float& s, uint32_t& id, uint32_t& ax, 
     }
 }
 
+// number of entries of sorted a[0..n) strictly less than (v, id)
+__device__ __forceinline__ uint32_t count_less(const Arr& a, uint32_t n, float v, uint32_t id) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (cless(a.sq[mid], a.id[mid], v, id))
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// merge path: how many of the first d outputs of merge(A[0..la), B[0..lb))
+// come from A (distinct (sq, id) keys, so the split is unique)
+__device__ __forceinline__ uint32_t merge_split(const Arr& A, uint32_t la, const Arr& B, uint32_t lb, uint32_t d) {
+    uint32_t lo = d > lb ? d - lb : 0u, hi = min(d, la);
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        const uint32_t bj = d - mid - 1;
+        if (cless(A.sq[mid], A.id[mid], B.sq[bj], B.id[bj]))
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
 // Sort n entries of `a` ascending by (sq, id) (distinct ids): 32-element
-// bitonic runs in registers, then merge passes where every element finds its
-// output slot by a binary search of the partner run. `t` is scratch of the
+// bitonic runs in registers, then merge passes: for runs of <= 64 every
+// element binary-searches its slot in the partner run; longer passes cut the
+// output of every run pair into 32-entry tiles; the lanes find the tiles' merge-path
+// splits in parallel (one binary search per 32 outputs), then each tile is
+// loaded as A-part ascending + B-part descending (a bitonic sequence) and
+// finished by a 5-step bitonic merge in registers. `t` is scratch of the
 // same capacity; returns whichever of a / t holds the result.
-__device__ Arr warp_sort(Arr a, Arr t, uint32_t n, int lane) {
+__device__ __noinline__ Arr warp_sort(Arr a, Arr t, uint32_t n, int lane) {
     for (uint32_t base = 0; base < n; base += 32) {
         const uint32_t i = base + lane;
         const bool v = i < n;
@@ -277,22 +296,89 @@ __device__ Arr warp_sort(Arr a, Arr t, uint32_t n, int lane) {
     }
     __syncwarp();
     Arr src = a, dst = t;
+    const uint32_t ntiles = (n + 31) / 32;
     for (uint32_t w = 32; w < n; w <<= 1) {
-        for (uint32_t i = lane; i < n; i += 32) {
-            const uint32_t start = i & ~(w - 1), pstart = start ^ w;
-            const float s = src.sq[i];
-            const uint32_t id = src.id[i], ax = src.aux[i];
-            uint32_t out = i;
-            if (pstart < n) {
-                Arr p;
-                p.id = src.id + pstart;
-                p.sq = src.sq + pstart;
-                p.aux = src.aux + pstart;
-                out = min(start, pstart) + (i - start) + count_less(p, min(w, n - pstart), s, id);
+        if (w <= 64) {  // short runs: every element binary-searches its partner run (<= 6 steps)
+            for (uint32_t i = lane; i < n; i += 32) {
+                const uint32_t start = i & ~(w - 1), pstart = start ^ w;
+                const float s = src.sq[i];
+                const uint32_t id = src.id[i], ax = src.aux[i];
+                uint32_t out = i;
+                if (pstart < n) {
+                    Arr p;
+                    p.id = src.id + pstart;
+                    p.sq = src.sq + pstart;
+                    p.aux = src.aux + pstart;
+                    out = min(start, pstart) + (i - start) + count_less(p, min(w, n - pstart), s, id);
+                }
+                dst.id[out] = id;
+                dst.sq[out] = s;
+                dst.aux[out] = ax;
             }
-            dst.id[out] = id;
-            dst.sq[out] = s;
-            dst.aux[out] = ax;
+            __syncwarp();
+            const Arr tmp = src;
+            src = dst;
+            dst = tmp;
+            continue;
+        }
+        for (uint32_t tb = 0; tb < ntiles; tb += 32) {
+            // this lane's tile: its run pair and merge-path splits
+            const uint32_t tt = tb + lane;
+            uint32_t ps = 0, la = 0, lb = 0, d0 = 0, d1 = 0, i0 = 0, i1 = 0;
+            if (tt < ntiles) {
+                const uint32_t o = tt * 32;
+                ps = o & ~(2 * w - 1);
+                la = min(w, n - ps);
+                lb = ps + w < n ? min(w, n - ps - w) : 0u;
+                d0 = o - ps;
+                d1 = min(d0 + 32, la + lb);
+                Arr A, B;
+                A.id = src.id + ps;
+                A.sq = src.sq + ps;
+                A.aux = src.aux + ps;
+                B.id = src.id + ps + w;
+                B.sq = src.sq + ps + w;
+                B.aux = src.aux + ps + w;
+                i0 = lb ? merge_split(A, la, B, lb, d0) : d0;
+                i1 = lb ? merge_split(A, la, B, lb, d1) : d1;
+            }
+            const uint32_t nt = min(32u, ntiles - tb);
+            for (uint32_t k = 0; k < nt; ++k) {
+                const uint32_t kps = __shfl_sync(FULL, ps, k), kd0 = __shfl_sync(FULL, d0, k);
+                const uint32_t kd1 = __shfl_sync(FULL, d1, k), ki0 = __shfl_sync(FULL, i0, k);
+                const uint32_t ki1 = __shfl_sync(FULL, i1, k);
+                const uint32_t na = ki1 - ki0, nb = (kd1 - kd0) - na, j0 = kd0 - ki0;
+                const uint32_t L = static_cast<uint32_t>(lane);
+                float s = CUDART_INF_F;
+                uint32_t id = EMPTY, ax = 0u;
+                uint32_t src_i = EMPTY;
+                if (L < na) src_i = kps + ki0 + L;                            // A ascending
+                else if (L >= 32u - nb) src_i = kps + w + j0 + (31u - L);     // B descending
+                if (src_i != EMPTY) {
+                    s = src.sq[src_i];
+                    id = src.id[src_i];
+                    ax = src.aux[src_i];
+                }
+#pragma unroll
+                for (int j = 16; j > 0; j >>= 1) {  // bitonic merge, ascending
+                    const float ps2 = __shfl_xor_sync(FULL, s, j);
+                    const uint32_t pid = __shfl_xor_sync(FULL, id, j);
+                    const uint32_t pax = __shfl_xor_sync(FULL, ax, j);
+                    const bool lower = (lane & j) == 0;
+                    const bool pless = cless(ps2, pid, s, id);
+                    if (lower ? pless : !pless) {
+                        s = ps2;
+                        id = pid;
+                        ax = pax;
+                    }
+                }
+                if (L < kd1 - kd0) {
+                    const uint32_t o = kps + kd0 + L;
+                    dst.id[o] = id;
+                    dst.sq[o] = s;
+                    dst.aux[o] = ax;
+                }
+            }
         }
         __syncwarp();
         const Arr tmp = src;
