@@ -66,8 +66,6 @@ constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint32_t EMPTY = 0xffffffffu;
 constexpr uint32_t VISITED = 0x80000000u;
 constexpr int XSTR = 36;        // floats per transposed chain row in the staging buffer
-constexpr int EXACT_ROWS = 4;   // rows per exact-distance batch (16 chain lanes)
-constexpr int FAST_ROWS = 8;    // rows per warp-tree batch
 
 __device__ __forceinline__ bool cless(float sa, uint32_t ia, float sb, uint32_t ib) {
     return sa < sb || (sa == sb && ia < ib);  // candidate_less, builder.hpp:23-25
@@ -445,7 +443,6 @@ struct TfbReg {
         deg = __shfl_sync(FULL, w_deg, slot);
     }
     __device__ uint32_t entry_id(uint32_t slot) const { return __shfl_sync(FULL, w_id, slot); }
-    __device__ uint32_t entry_deg(uint32_t slot) const { return __shfl_sync(FULL, w_deg, slot); }
     __device__ void set_visited(uint32_t slot, int lane) {
         if (static_cast<uint32_t>(lane) == slot) w_vis = true;
     }
@@ -679,7 +676,6 @@ struct TfbMem {
         deg = W.aux[slot] & ~VISITED;
     }
     __device__ uint32_t entry_id(uint32_t slot) const { return W.id[slot]; }
-    __device__ uint32_t entry_deg(uint32_t slot) const { return W.aux[slot] & ~VISITED; }
     __device__ void set_visited(uint32_t slot, int lane) {
         const uint32_t a = W.aux[slot];
         __syncwarp();
