@@ -918,6 +918,77 @@ __device__ void dist_exact(const SearchLaunch& P, Common& c, uint32_t items, uin
     }
 }
 
+// dist_exact for a compile-time chunk count with two chunks of look-ahead
+// (three rotating register buffers): the next-but-one chunk's loads are in
+// flight while the current chunk's chains run
+template <int NCH>
+__device__ void dist_exact_la2(const SearchLaunch& P, Common& c, uint32_t items, uint32_t w, int lane) {
+    static_assert(NCH >= 2, "two chunks of look-ahead");
+    const IndexView& ix = P.ix;
+    constexpr uint32_t DS = 128u * NCH;
+    const int cr = lane >> 2, cc = lane & 3;
+    uint32_t rest = items;
+    while (rest) {
+        int jr[4];
+        const int nb = take_batch(rest, jr);
+        const float* rp[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uint32_t wr = __shfl_sync(FULL, w, r < nb ? jr[r] : jr[0]);
+            rp[r] = ix.rows + static_cast<uint64_t>(wr) * DS + 4u * lane;
+        }
+        float acc = 0.0f;
+        float4 buf[3][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            buf[0][r] = ldg_f4(rp[r]);
+            buf[1][r] = ldg_f4(rp[r] + 128u);
+        }
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+            if (ch + 2 < NCH) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) buf[(ch + 2) % 3][r] = ldg_f4(rp[r] + 128u * (ch + 2));
+            }
+            const float4 qv = *reinterpret_cast<const float4*>(c.q + 128u * ch + 4u * lane);
+            float* st = c.stage + lane;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                if (r < nb) {
+                    const float4 v = buf[ch % 3][r];
+                    const float2 lo = sq2(make_float2(v.x, v.y), make_float2(qv.x, qv.y));
+                    const float2 hi = sq2(make_float2(v.z, v.w), make_float2(qv.z, qv.w));
+                    st[(r * 4 + 0) * XSTR] = lo.x;
+                    st[(r * 4 + 1) * XSTR] = lo.y;
+                    st[(r * 4 + 2) * XSTR] = hi.x;
+                    st[(r * 4 + 3) * XSTR] = hi.y;
+                }
+            }
+            __syncwarp();
+            if (cr < nb) {
+                const float* sp = c.stage + (cr * 4 + cc) * XSTR;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const float4 x = *reinterpret_cast<const float4*>(sp + 4 * i);
+                    acc = __fadd_rn(acc, x.x);
+                    acc = __fadd_rn(acc, x.y);
+                    acc = __fadd_rn(acc, x.z);
+                    acc = __fadd_rn(acc, x.w);
+                }
+            }
+            __syncwarp();
+        }
+        const float a1 = __shfl_down_sync(FULL, acc, 1);
+        const float a2 = __shfl_down_sync(FULL, acc, 2);
+        const float a3 = __shfl_down_sync(FULL, acc, 3);
+        int jmine = jr[0];
+#pragma unroll
+        for (int r = 1; r < 4; ++r)
+            if (r == cr) jmine = jr[r];
+        if (cc == 0 && cr < nb) c.sqbuf[jmine] = __fadd_rn(__fadd_rn(acc, a1), __fadd_rn(a2, a3));
+    }
+}
+
 // Warp-tree distances, two rows at a time: each half-warp owns one row and
 // every lane issues all of its 2*NCH float4 loads back to back (one memory
 // latency per row pair instead of one per 128-float chunk), then a 16-lane
@@ -1108,6 +1179,8 @@ __device__ __forceinline__ void distances(const SearchLaunch& P, Common& c, uint
         if constexpr (NCH > 0 && NCH <= 6) {
             if (P.tune & 64u)  // row-pair variant (measured slower: serial chains per pair)
                 dist_exact_pairs<NCH>(P, c, items, w, lane);
+            else if constexpr (NCH >= 2)
+                dist_exact_la2<(NCH >= 2 ? NCH : 2)>(P, c, items, w, lane);
             else
                 dist_exact<NCH>(P, c, items, w, lane);
         } else {

@@ -44,6 +44,16 @@ FIXTURES = {
     # degree cap 64 (two 32-edge groups per expansion)
     "deg64": (dict(n=3000, d=16, centres=20, sigma=0.5, unit=False, metric="euclidean"),
               dict(M=32, efC=120, seed=9)),
+    # the benchmark shapes' compile-time distance kernels (padded_dim = 128 x NCH):
+    # unit-normalised mixtures like cfg-2/3/4 at a few thousand points
+    "unit256": (dict(n=1500, d=256, centres=16, sigma=0.4, unit=True, metric="euclidean"),
+                dict(M=16, efC=100, seed=11)),
+    "unit512": (dict(n=1200, d=512, centres=16, sigma=0.4, unit=True, metric="euclidean"),
+                dict(M=16, efC=100, seed=13)),
+    "unit768": (dict(n=1200, d=768, centres=16, sigma=0.4, unit=True, metric="euclidean"),
+                dict(M=16, efC=100, seed=15)),
+    "unit1024": (dict(n=1000, d=1024, centres=16, sigma=0.3, unit=True, metric="euclidean"),
+                 dict(M=16, efC=100, seed=17)),
 }
 
 

@@ -350,3 +350,24 @@ def test_async_submit_wait_matches_sync(pag, built):
     pb = cos.search_submit(bad, pag.SearchParams(K=5, efS=20))
     with pytest.raises(ValueError, match="zero query under cosine metric"):
         pb.wait()
+
+
+@pytest.mark.parametrize("name", ["unit256", "unit512", "unit768", "unit1024"])
+def test_benchmark_shapes_bitexact_and_fast(pag, built, name):
+    """The compile-time distance kernels the benchmarks run (padded_dim =
+    128 x NCH, NCH = 2/4/6/8): reference-order mode bit-exact against the
+    oracle (register and memory TFB layouts, both occupancy flavours), and
+    warp-tree mode within the north-star tolerance."""
+    fx = built(name)
+    for K, efS in ((10, 40), (10, 300), (100, 150)):
+        check_bitexact(pag, fx, K, efS)
+    ix = gpu_index(pag, fx["index"])
+    gi, gs = O.ground_truth(fx["base"], fx["queries"], 10)
+    a = ix.search_batch(fx["queries"], pag.SearchParams(K=10, efS=60, exact_dist=False))
+    b = O.OracleIndex(fx["index"]).search(fx["queries"], 10, 60)
+    same = np.mean([set(a.ids[i, :a.n_out[i]]) == set(b[0][i, :b[2][i]]) for i in range(len(a.n_out))])
+    assert same >= 0.99
+    both = a.ids == b[0]
+    rel = np.abs(a.sq - b[1]) / np.maximum(np.abs(b[1]), 1e-30)
+    assert rel[both].max() <= 1e-5
+    assert abs(pag.mean_recall(a.ids, a.n_out, gi, gs, 10) - pag.mean_recall(b[0], b[2], gi, gs, 10)) <= 0.002
