@@ -591,8 +591,9 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     };
     // per-warp budget that keeps the kernel's resident-block bound (4 or 6
     // blocks of 4 warps in 228 KB) reachable
-    const uint64_t budget = pagdev::search_high_occupancy(L) ? std::min<uint32_t>(kWarpSmemBudget, 9 * 1024)
-                                                             : kWarpSmemBudget;
+    uint64_t budget = pagdev::search_high_occupancy(L) ? std::min<uint32_t>(kWarpSmemBudget, 9 * 1024)
+                                                       : kWarpSmemBudget;
+    if (const char* e = std::getenv("PAG_GPU_SMEM_BUDGET")) budget = std::strtoull(e, nullptr, 10);  // tests
     if (total() > budget) rl_s = false;
     if (total() > budget) m_s = false;
     if (total() > budget) r_s = false;
@@ -627,6 +628,10 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     if (bps <= 0) throw_err(PAG_GPU_ERUNTIME, "search configuration does not fit on the GPU");
     const int want_blocks = static_cast<int>((nq + kWarpsPerBlock - 1) / kWarpsPerBlock);
     pl.grid = std::max(1, std::min(r.num_sms * bps, want_blocks));
+    if (std::getenv("PAG_GPU_DEBUG"))
+        std::fprintf(stderr, "[pag_gpu] plan: b=%u warps/block=%d blocks/SM=%d grid=%d smem/warp=%u W/rings/RL/merge in smem %u%u%u%u\n",
+                     L.b, L.warps_per_block, bps, pl.grid, L.warp_smem_bytes, L.W_in_smem, L.rings_in_smem,
+                     L.rl_in_smem, L.merge_in_smem);
     return pl;
 }
 

@@ -371,3 +371,32 @@ def test_benchmark_shapes_bitexact_and_fast(pag, built, name):
     rel = np.abs(a.sq - b[1]) / np.maximum(np.abs(b[1]), 1e-30)
     assert rel[both].max() <= 1e-5
     assert abs(pag.mean_recall(a.ids, a.n_out, gi, gs, 10) - pag.mean_recall(b[0], b[2], gi, gs, 10)) <= 0.002
+
+
+def test_working_set_off_chip_is_exact(pag, built, monkeypatch):
+    """b > 32 with a per-warp smem budget too small for the working set: W,
+    the rings, R_L and the merge buffer all live in the warp's HBM scratch.
+    Bit-identical to the oracle, for queries and the construction search."""
+    monkeypatch.setenv("PAG_GPU_SMEM_BUDGET", "2048")
+    for name, K, efS, kw in (("euc48", 100, 300, {}), ("euc48", 250, 500, {}), ("deg64", 64, 128, {}),
+                             ("deg64", 10, 700, dict(b_override=48)), ("cos20", 33, 70, {})):
+        fx = built(name)
+        ix = pag.load_index(fx["index"])
+        try:
+            got = ix.search_batch(fx["queries"], pag.SearchParams(K=K, efS=efS, **kw))
+            want = O.OracleIndex(fx["index"]).search(fx["queries"], K, efS, **kw)
+            assert_same_results((got.ids, got.sq, got.n_out, got.stats), want, f"off-chip {name} {K}/{efS} {kw}")
+        finally:
+            ix.close()
+    fx = built("deg64")
+    ix = pag.load_index(fx["index"])
+    try:
+        oix = O.OracleIndex(fx["index"])
+        nodes = np.arange(0, oix.n, 7, dtype=np.uint32)
+        kw = dict(K=64, efS=300, b_override=48)
+        got = ix.construction_search(nodes, pag.SearchParams(**kw), collect_pes=True)
+        want = oix.construction_search(nodes, collect_pes=True, **kw)
+        assert_same_results((got.ids, got.sq, got.n_out, got.stats), want[:4], "off-chip construction")
+        assert np.array_equal(got.pes_n, want[5])
+    finally:
+        ix.close()
