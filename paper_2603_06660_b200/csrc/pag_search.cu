@@ -483,6 +483,33 @@ struct TfbReg {
         if (rf_size < b) ++rf_size;
         else rf_head = (rf_head + 1 == b) ? 0 : rf_head + 1;
     }
+    // push_fp of the lanes in pm, in lane order (lane l supplies its entry):
+    // element i lands in physical slot (head + size + i) mod b, the last
+    // element on a slot wins, as the sequential overwrite-oldest pushes
+    __device__ void push_fp_many(uint32_t pm, uint32_t id, float sq, uint32_t deg, int lane) {
+        const uint32_t np = __popc(pm);
+        uint32_t start = rf_head + rf_size;
+        if (start >= b) start -= b;
+        const uint32_t L = static_cast<uint32_t>(lane);
+        const uint32_t d = L >= start ? L - start : L + b - start;
+        const bool upd = L < b && d < np;
+        uint32_t src = 0;
+        if (upd) src = __fns(pm, 0, static_cast<int>(d + b * ((np - 1 - d) / b)) + 1);
+        const uint32_t nid = __shfl_sync(FULL, id, src), ndeg = __shfl_sync(FULL, deg, src);
+        const float nsq = __shfl_sync(FULL, sq, src);
+        if (upd) {
+            f_id = nid;
+            f_sq = nsq;
+            f_deg = ndeg;
+        }
+        const uint32_t tot = rf_size + np;
+        if (tot <= b) {
+            rf_size = tot;
+        } else {
+            rf_head = (rf_head + tot - b) % b;
+            rf_size = b;
+        }
+    }
     // routing.cpp:55-69
     __device__ void admit(uint32_t id, float sq, uint32_t deg, int lane) {
         if (wsize < b) {
@@ -724,6 +751,25 @@ struct TfbMem {
     }
     __device__ void push_fp(uint32_t id, float sq, uint32_t deg, int lane) {
         ring_push(rf, b, rf_head, rf_size, id, sq, deg, lane);
+        __syncwarp();
+    }
+    // push_fp of the lanes in pm in lane order; b > 32 >= popc(pm), so no two
+    // pushes of one call share a slot
+    __device__ void push_fp_many(uint32_t pm, uint32_t id, float sq, uint32_t deg, int lane) {
+        if ((pm >> lane) & 1u) {
+            uint32_t pos = rf_head + rf_size + __popc(pm & ((1u << lane) - 1u));
+            while (pos >= b) pos -= b;
+            rf.id[pos] = id;
+            rf.sq[pos] = sq;
+            rf.aux[pos] = deg;
+        }
+        const uint32_t tot = rf_size + __popc(pm);
+        if (tot <= b) {
+            rf_size = tot;
+        } else {
+            rf_head = (rf_head + tot - b) % b;
+            rf_size = b;
+        }
         __syncwarp();
     }
     __device__ void admit(uint32_t id, float sq, uint32_t deg, int lane) {
@@ -1362,9 +1408,42 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
         if (surv) distances<EXACT, NCH>(P, c, surv, w, lane);
         PT(5);
 
-        // (iv) in-order replay with the live radius
+        // (iv) in-order replay with the live radius, one step per admission:
+        // every remaining survivor is re-tested in parallel at the current
+        // radius; the passes before the first admissible one go to R_F in
+        // order (the radius cannot change before it), that one is admitted
+        // (the radius shrinks) and the rest are re-tested
         uint32_t passed = 0;
-        uint32_t rem = surv;
+        if (!any_dup && !(P.tune & 8u)) {
+            const float sqv = spec ? c.sqbuf[lane] : 0.0f;
+            const uint32_t dgv = spec ? c.degbuf[lane] : 0u;
+            uint32_t rem = surv;
+            while (rem) {
+                const float adist = s.admission_dist(), asq = s.admission_sq();
+                bool pl = false;
+                if ((rem >> lane) & 1u) {
+                    if (exact_mode) {
+                        pl = true;
+                    } else {
+                        const float tau = adist == adist0 ? tau0 : prt_threshold(en, duq, adist);
+                        pl = tau < TAU_HI && (tau <= -1.0f || quot >= tau);
+                    }
+                }
+                const uint32_t pm = __ballot_sync(FULL, pl);
+                const uint32_t am = __ballot_sync(FULL, pl && sqv < asq);
+                const uint32_t fp = pm & (am ? (am & (0u - am)) - 1u : 0xffffffffu);
+                if (fp) s.push_fp_many(fp, w, sqv, dgv, lane);
+                passed |= fp;
+                if (!am) break;
+                const int k = __ffs(am) - 1;
+                s.admit(__shfl_sync(FULL, w, k), __shfl_sync(FULL, sqv, k), __shfl_sync(FULL, dgv, k), lane);
+                passed |= 1u << k;
+                rem &= ~((2u << k) - 1u);
+            }
+            c.n_pass += __popc(passed);
+            c.n_exact += __popc(passed);
+        }
+        uint32_t rem = (!any_dup && !(P.tune & 8u)) ? 0u : surv;  // sequential replay (duplicates, diagnostics)
         while (rem) {
             const int jl = __ffs(rem) - 1;
             rem &= rem - 1;
