@@ -78,7 +78,9 @@ int pag_gpu_close(pag_gpu_index* ix);
 /* info[0..11] = n, dim, padded_dim, L, m, M, metric (0 euclidean, 1 cosine),
  * n_entries, seed, total_edges, n_devices, device_bytes_per_replica;
  * info[12] = tensor-core ground-truth queries re-run exactly so far;
- * info[13..15] = the header's efC, b_build, enable_pes.
+ * info[13..15] = the header's efC, b_build, enable_pes;
+ * info[16] = nodes that repeat a target inside one 32-edge group (0 lets
+ * the search skip its in-group duplicate resolution).
  * Replaces the PagIndex/VectorSet accessors (builder.hpp:71-91). */
 int pag_gpu_info(const pag_gpu_index* ix, uint64_t* info, size_t n_info);
 

@@ -45,6 +45,9 @@ struct IndexView {
     uint32_t slot_stride, cwp, block_bytes;
     uint32_t n_entries;
     uint32_t cosine;
+    // no node repeats a target inside a 32-edge group (checked on the device
+    // after load and refresh): the search skips its duplicate resolution
+    uint32_t dup_free;
 };
 
 // One batched search launch.
@@ -157,6 +160,9 @@ cudaError_t launch_gt_tc(const GtTcLaunch& g, cudaStream_t stream);
 // pag_util.cu: staged node blocks -> their slots in the adjacency array
 cudaError_t scatter_blocks(const void* staging, const uint32_t* ids, uint32_t count, void* adj,
                            uint32_t block_bytes, cudaStream_t stream);
+// nodes with a target repeated inside one 32-edge group -> *count_dev
+cudaError_t count_dup_groups(const void* adj, const uint32_t* deg, uint64_t n, uint32_t block_bytes,
+                             uint32_t* count_dev, cudaStream_t stream);
 size_t gt_tc_smem_bytes();
 uint32_t gt_tc_cmax();
 uint32_t gt_tc_block_n();

@@ -232,6 +232,7 @@ struct pag_gpu_index {
     std::vector<uint32_t> entries;
     uint32_t maxdeg = 0, cb = 0, cwp = 0, slot_stride = 0, block_bytes = 0, sub_dim = 0;
     uint64_t total_edges = 0;
+    uint32_t dup_nodes = 1;        // nodes repeating a target inside a 32-edge group (0: fast path)
     float max_bnorm = 0.0f;        // max squared row norm
     uint64_t gt_uncertified = 0;   // tensor-core GT queries re-run exactly (diagnostic)
     // host mirror of the device adjacency + degrees (built at the first refresh)
@@ -260,6 +261,7 @@ struct pag_gpu_index {
         v.block_bytes = block_bytes;
         v.n_entries = static_cast<uint32_t>(entries.size());
         v.cosine = metric == 1;
+        v.dup_free = dup_nodes == 0;
         return v;
     }
 };
@@ -1254,6 +1256,26 @@ void check_status(uint32_t so) {
     if (so & pagdev::kStatusVisitedOverflow) throw_err(PAG_GPU_ERUNTIME, "visited set overflow after retries");
 }
 
+// ix.dup_nodes from the first replica's adjacency (after load / refresh)
+static void update_dup_nodes(pag_gpu_index& ix) {
+    if (ix.reps.empty()) return;
+    Replica& r = ix.reps[0];
+    cuda_check(cudaSetDevice(r.device), "cudaSetDevice");
+    uint32_t* cnt = nullptr;
+    dev_alloc(&cnt, 4);
+    uint32_t h = 1;
+    const bool dbg = std::getenv("PAG_GPU_DEBUG") != nullptr;
+    if (dbg) std::fprintf(stderr, "[pag_gpu] dup check: n=%llu block_bytes=%u\n", (unsigned long long)ix.n, ix.block_bytes);
+    cudaError_t e = pagdev::count_dup_groups(r.adj, r.deg, ix.n, ix.block_bytes, cnt, r.stream);
+    if (dbg) std::fprintf(stderr, "[pag_gpu] dup kernel launched: %d\n", (int)e);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(r.stream);
+    if (dbg) std::fprintf(stderr, "[pag_gpu] dup kernel done: %d\n", (int)e);
+    if (e == cudaSuccess) e = cudaMemcpy(&h, cnt, 4, cudaMemcpyDeviceToHost);
+    dev_free(cnt);
+    cuda_check(e, "duplicate-target check");
+    ix.dup_nodes = h;
+}
+
 extern "C" {
 
 void pag_gpu_default_params(pag_search_params* p) {
@@ -1271,6 +1293,7 @@ int pag_gpu_open(const char* index_path, uint32_t device_mask, pag_gpu_index** o
         if (!out || !index_path) throw_err(PAG_GPU_EINVAL, "null argument");
         *out = nullptr;
         auto ix = open_index(index_path, device_mask);
+        update_dup_nodes(*ix);
         *out = ix.release();
     });
 }
@@ -1301,6 +1324,7 @@ int pag_gpu_refresh(pag_gpu_index* ix, const char* index_path, uint64_t* stats) 
         if (!ix || !index_path) throw_err(PAG_GPU_EINVAL, "null argument");
         std::lock_guard<std::mutex> g(ix->mu);
         refresh_index(*ix, index_path, stats);
+        update_dup_nodes(*ix);
     });
 }
 
@@ -1315,11 +1339,11 @@ int pag_gpu_close(pag_gpu_index* ix) {
 int pag_gpu_info(const pag_gpu_index* ix, uint64_t* info, size_t n_info) {
     return guarded([&] {
         if (!ix || !info) throw_err(PAG_GPU_EINVAL, "null argument");
-        const uint64_t v[16] = {ix->n, ix->dim, ix->padded, ix->L, ix->m, ix->M, ix->metric,
+        const uint64_t v[17] = {ix->n, ix->dim, ix->padded, ix->L, ix->m, ix->M, ix->metric,
                                 ix->entries.size(), ix->seed, ix->total_edges, ix->reps.size(),
                                 ix->reps.empty() ? 0 : ix->reps[0].bytes, ix->gt_uncertified,
-                                ix->efC, ix->b_build, ix->enable_pes};
-        for (size_t i = 0; i < n_info && i < 16; ++i) info[i] = v[i];
+                                ix->efC, ix->b_build, ix->enable_pes, ix->dup_nodes};
+        for (size_t i = 0; i < n_info && i < 17; ++i) info[i] = v[i];
     });
 }
 

@@ -1382,10 +1382,15 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
         const uint32_t cand_mask = __ballot_sync(FULL, cand);
         // duplicate targets inside the group (reference order: a later copy
         // is skipped when an earlier copy passed and marked it)
-        const unsigned long long key =
-            cand ? static_cast<unsigned long long>(w) : ((1ull << 32) | static_cast<unsigned>(lane));
-        const uint32_t same = __match_any_sync(FULL, key) & cand_mask;
-        const bool any_dup = __any_sync(FULL, __popc(same) > 1);
+        // (none in an index whose groups are all duplicate-free: ix.dup_free)
+        uint32_t same = cand ? 1u << lane : 0u;
+        bool any_dup = false;
+        if (!ix.dup_free) {
+            const unsigned long long key =
+                cand ? static_cast<unsigned long long>(w) : ((1ull << 32) | static_cast<unsigned>(lane));
+            same = __match_any_sync(FULL, key) & cand_mask;
+            any_dup = __any_sync(FULL, __popc(same) > 1);
+        }
 
         const bool spec = cand && pass0;
         if (track_pes) {  // every edge, marked or not; quot does not depend on the radius

@@ -18,7 +18,36 @@ __global__ void scatter_blocks_kernel(const uint4* __restrict__ staging, const u
     }
 }
 
+// nodes whose adjacency repeats a target inside one 32-edge group (one warp
+// per node; lane j holds edge g0 + j, as the search kernel does)
+__global__ void dup_groups_kernel(const uint8_t* __restrict__ adj, const uint32_t* __restrict__ deg, uint64_t n,
+                                  uint32_t block_bytes, uint32_t* __restrict__ count) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t u = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; u < n; u += warps) {
+        const uint32_t d = deg[u];
+        const uint32_t* tg = reinterpret_cast<const uint32_t*>(adj + u * block_bytes);
+        bool dup = false;
+        for (uint32_t g0 = 0; g0 < d; g0 += 32) {
+            const bool act = g0 + lane < d;
+            const unsigned long long key = act ? static_cast<unsigned long long>(tg[g0 + lane])
+                                               : ((1ull << 32) | lane);
+            const uint32_t same = __match_any_sync(0xffffffffu, key);  // all lanes (no short-circuit)
+            dup |= act && __popc(same) > 1;
+        }
+        if (__any_sync(0xffffffffu, dup) && lane == 0) atomicAdd(count, 1u);
+    }
+}
+
 }  // namespace
+
+cudaError_t count_dup_groups(const void* adj, const uint32_t* deg, uint64_t n, uint32_t block_bytes,
+                             uint32_t* count_dev, cudaStream_t stream) {
+    cudaError_t e = cudaMemsetAsync(count_dev, 0, 4, stream);
+    if (e != cudaSuccess || n == 0) return e;
+    dup_groups_kernel<<<148 * 8, 256, 0, stream>>>(static_cast<const uint8_t*>(adj), deg, n, block_bytes, count_dev);
+    return cudaGetLastError();
+}
 
 cudaError_t scatter_blocks(const void* staging, const uint32_t* ids, uint32_t count, void* adj,
                            uint32_t block_bytes, cudaStream_t stream) {

@@ -265,6 +265,13 @@ class PagIndex:
         return {"new_nodes": int(st[0]), "changed_blocks": int(st[1]), "bytes_uploaded": int(st[2]),
                 "seconds": int(st[3]) / 1e6}
 
+    def dup_nodes(self) -> int:
+        """Nodes repeating a target inside one 32-edge group (0: the search
+        skips its in-group duplicate resolution)."""
+        info = np.zeros(17, np.uint64)
+        check(lib.pag_gpu_info(self._h, info, 17))
+        return int(info[16])
+
     def gt_uncertified(self) -> int:
         """Tensor-core ground-truth queries that failed the certificate and were re-run exactly."""
         info = np.zeros(13, np.uint64)

@@ -400,3 +400,49 @@ def test_working_set_off_chip_is_exact(pag, built, monkeypatch):
         assert np.array_equal(got.pes_n, want[5])
     finally:
         ix.close()
+
+
+def _with_duplicate_targets(src: str, dst: str, every: int = 7) -> int:
+    """Copy a PAGIDX01 file, overwriting edge 2 of every `every`-th node with
+    its edge 0 (same target, scalars and codes): targets repeated inside a
+    32-edge group. Returns the number of patched nodes."""
+    import struct
+    data = bytearray(open(src, "rb").read())
+    n = struct.unpack_from("<Q", data, 12)[0]
+    L = struct.unpack_from("<I", data, 28)[0]
+    n_entries = struct.unpack_from("<I", data, 62)[0]
+    rec = 4 + (L + 1) // 2 + 12
+    off = 66 + 4 * n_entries
+    patched = 0
+    for u in range(n):
+        deg = struct.unpack_from("<I", data, off)[0]
+        e0 = off + 4
+        if u % every == 0 and deg >= 3:
+            data[e0 + 2 * rec:e0 + 3 * rec] = data[e0:e0 + rec]
+            patched += 1
+        off = e0 + deg * rec
+    open(dst, "wb").write(bytes(data))
+    return patched
+
+
+def test_duplicate_targets_in_group_bitexact(pag, built, tmp_path):
+    """An index whose adjacency repeats targets inside a group (the loader
+    accepts it; routing.cpp:160-183 skips a copy once an earlier one passed
+    and was marked): the search takes its duplicate-resolution path and stays
+    bit-identical to the oracle; a duplicate-free index reports 0 such nodes
+    and takes the fast path."""
+    fx = built("euc48")
+    dup_path = str(tmp_path / "dup.pagidx")
+    assert _with_duplicate_targets(fx["index"], dup_path) > 0
+    clean = gpu_index(pag, fx["index"])
+    assert clean.dup_nodes() == 0
+    ix = pag.load_index(dup_path)
+    try:
+        assert ix.dup_nodes() > 0
+        oix = O.OracleIndex(dup_path)
+        for K, efS in ((10, 40), (10, 200), (100, 300)):
+            got = ix.search_batch(fx["queries"], pag.SearchParams(K=K, efS=efS))
+            want = oix.search(fx["queries"], K, efS)
+            assert_same_results((got.ids, got.sq, got.n_out, got.stats), want, f"duplicates {K}/{efS}")
+    finally:
+        ix.close()
