@@ -584,8 +584,9 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     L.off_stage = off;
     if (p.exact_dist) off = align16(off + 4 * 36 * 16);  // transposed chain staging (exact mode only)
     // movable regions: W (12b), rings (24b), R_L (24 capr), merge (48b);
-    // with b <= 32 the working set and rings live in registers
-    const uint64_t szW = regs ? 0 : align16(12 * b), szR = regs ? 0 : align16(24 * b),
+    // with b <= 32 the working set and R_T live in registers
+    // (b <= 32: the rings region holds R_F only, 32 slots; R_T is in registers)
+    const uint64_t szW = regs ? 0 : align16(12 * b), szR = regs ? 12 * 32 : align16(24 * b),
                    szRL = align16(24 * capr), szM = align16(48 * b);
     bool w_s = true, r_s = true, rl_s = true, m_s = true;
     auto total = [&]() {

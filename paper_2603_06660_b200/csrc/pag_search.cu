@@ -395,15 +395,17 @@ struct TfbReg {
     uint32_t w_id, w_deg;
     float w_sq;
     bool w_vis;
-    uint32_t f_id, f_deg;
-    float f_sq;
+    Arr rf;  // ring R_F: b <= 32 slots in smem (bulk pushes scatter into it)
     uint32_t t_id, t_deg;
     float t_sq;
     uint32_t wsize, rf_head, rf_size, rt_head, rt_size;
     float zmax_sq, zmax_dist;
     uint32_t zmax_idx;
 
-    __device__ void init(uint32_t b_, uint8_t*, uint8_t*, const SearchLaunch&) { b = b_; }
+    __device__ void init(uint32_t b_, uint8_t* sw, uint8_t* gw, const SearchLaunch& P) {
+        b = b_;
+        rf = make_arr((P.rings_in_smem ? sw : gw) + P.off_rf, 32);
+    }
     __device__ void reset() {
         wsize = rf_head = rf_size = rt_head = rt_size = 0;
         zmax_sq = zmax_dist = 0.0f;
@@ -475,40 +477,41 @@ struct TfbReg {
     __device__ void push_fp(uint32_t id, float sq, uint32_t deg, int lane) {  // routing.hpp:128
         uint32_t pos = rf_head + rf_size;
         if (pos >= b) pos -= b;
-        if (static_cast<uint32_t>(lane) == pos) {
-            f_id = id;
-            f_sq = sq;
-            f_deg = deg;
+        if (lane == 0) {
+            rf.id[pos] = id;
+            rf.sq[pos] = sq;
+            rf.aux[pos] = deg;
         }
         if (rf_size < b) ++rf_size;
         else rf_head = (rf_head + 1 == b) ? 0 : rf_head + 1;
+        __syncwarp();
     }
     // push_fp of the lanes in pm, in lane order (lane l supplies its entry):
-    // element i lands in physical slot (head + size + i) mod b, the last
-    // element on a slot wins, as the sequential overwrite-oldest pushes
+    // element i lands in slot (head + size + i) mod b; when a call wraps the
+    // ring, only the last element aimed at a slot writes it (the sequential
+    // overwrite-oldest pushes keep that one)
     __device__ void push_fp_many(uint32_t pm, uint32_t id, float sq, uint32_t deg, int lane) {
         const uint32_t np = __popc(pm);
-        uint32_t start = rf_head + rf_size;
-        if (start >= b) start -= b;
-        const uint32_t L = static_cast<uint32_t>(lane);
-        const uint32_t d = L >= start ? L - start : L + b - start;
-        const bool upd = L < b && d < np;
-        uint32_t src = 0;
-        if (upd) src = __fns(pm, 0, static_cast<int>(d + b * ((np - 1 - d) / b)) + 1);
-        const uint32_t nid = __shfl_sync(FULL, id, src), ndeg = __shfl_sync(FULL, deg, src);
-        const float nsq = __shfl_sync(FULL, sq, src);
-        if (upd) {
-            f_id = nid;
-            f_sq = nsq;
-            f_deg = ndeg;
+        if ((pm >> lane) & 1u) {
+            const uint32_t r = __popc(pm & ((1u << lane) - 1u));
+            if (r + b >= np) {
+                uint32_t pos = rf_head + rf_size + r;
+                while (pos >= b) pos -= b;
+                rf.id[pos] = id;
+                rf.sq[pos] = sq;
+                rf.aux[pos] = deg;
+            }
         }
         const uint32_t tot = rf_size + np;
         if (tot <= b) {
             rf_size = tot;
         } else {
-            rf_head = (rf_head + tot - b) % b;
+            uint32_t h = rf_head + (tot - b);
+            while (h >= b) h -= b;
+            rf_head = h;
             rf_size = b;
         }
+        __syncwarp();
     }
     // routing.cpp:55-69
     __device__ void admit(uint32_t id, float sq, uint32_t deg, int lane) {
@@ -541,6 +544,13 @@ struct TfbReg {
         wsize = 0;
         const uint32_t L = static_cast<uint32_t>(lane);
         const bool fv = L < b && ((L + b - rf_head) % b) < rf_size;
+        uint32_t f_id = 0, f_deg = 0;
+        float f_sq = 0.0f;
+        if (L < b) {
+            f_id = rf.id[L];
+            f_sq = rf.sq[L];
+            f_deg = rf.aux[L];
+        }
         const bool tv = L < b && ((L + b - rt_head) % b) < rt_size;
         const uint32_t nm = rf_size + rt_size;
         rf_head = rf_size = rt_head = rt_size = 0;
@@ -767,7 +777,9 @@ struct TfbMem {
         if (tot <= b) {
             rf_size = tot;
         } else {
-            rf_head = (rf_head + tot - b) % b;
+            uint32_t h = rf_head + (tot - b);
+            while (h >= b) h -= b;
+            rf_head = h;
             rf_size = b;
         }
         __syncwarp();
