@@ -566,6 +566,7 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     // on-chip table and a small one keeps occupancy (W is on-chip)
     L.hash_log2 = p.efS <= 200 ? 10 : 8;
     if (const char* e = std::getenv("PAG_GPU_HASH_LOG2")) L.hash_log2 = static_cast<uint32_t>(std::atoi(e));
+    L.hash_log2 = std::max(3u, std::min(16u, L.hash_log2));  // >= 2 buckets of 4 slots
     const uint32_t b = L.b;
     L.rl_cap = L.r_max * b + b;  // every W flush of a query (r_max - 1 end_rounds + the final flush)
     const uint32_t capr = L.rl_cap;

@@ -140,40 +140,44 @@ struct Common {
 
 };
 
-__device__ __forceinline__ bool marked(const Common& c, uint32_t id) {
-    const uint32_t mask = (1u << c.hs_log2) - 1;
-    uint32_t h = hslot(id, c.hs_log2);
+// The smem visited table is bucketed: 4-slot buckets (one 16-B load), an id
+// hashes to a bucket, inserts take the bucket's first empty slot (atomicCAS
+// in slot order) or move on to the next bucket. Slots fill in order and are
+// never freed, so a bucket with an empty slot ends the probe.
+__device__ __forceinline__ bool hash_has(const Common& c, uint32_t id) {
+    const uint32_t bmask = (1u << (c.hs_log2 - 2)) - 1;
+    uint32_t bk = hslot(id, c.hs_log2 - 2);
     while (true) {
-        const uint32_t v = c.hs[h];
-        if (v == id) return true;
-        if (v == EMPTY) break;
-        h = (h + 1) & mask;
+        const uint4 v = reinterpret_cast<const uint4*>(c.hs)[bk];
+        if (v.x == id || v.y == id || v.z == id || v.w == id) return true;
+        if (v.w == EMPTY) return false;  // (slots fill in order: w empty <=> some empty)
+        bk = (bk + 1) & bmask;
     }
+}
+
+__device__ __forceinline__ bool marked(const Common& c, uint32_t id) {
+    if (hash_has(c, id)) return true;
     if (!c.gt_used) return false;
     return (c.gbm[id >> 5] >> (id & 31u)) & 1u;
 }
 
-// the smem part of marked(): open-addressing probe only
-__device__ __forceinline__ bool hash_has(const Common& c, uint32_t id) {
-    const uint32_t mask = (1u << c.hs_log2) - 1;
-    uint32_t h = hslot(id, c.hs_log2);
+// one id into the table (the caller keeps the load at most half)
+__device__ __forceinline__ void hash_insert(const Common& c, uint32_t id) {
+    const uint32_t bmask = (1u << (c.hs_log2 - 2)) - 1;
+    uint32_t bk = hslot(id, c.hs_log2 - 2);
     while (true) {
-        const uint32_t v = c.hs[h];
-        if (v == id) return true;
-        if (v == EMPTY) return false;
-        h = (h + 1) & mask;
+        uint32_t* b4 = c.hs + 4 * bk;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (atomicCAS(b4 + k, EMPTY, id) == EMPTY) return;
+        bk = (bk + 1) & bmask;
     }
 }
 
 // warp-uniform call; lane 0 writes
 __device__ __forceinline__ void mark(Common& c, uint32_t id, int lane) {
     if (c.hs_count < (1u << c.hs_log2) / 2) {
-        if (lane == 0) {
-            const uint32_t mask = (1u << c.hs_log2) - 1;
-            uint32_t h = hslot(id, c.hs_log2);
-            while (c.hs[h] != EMPTY) h = (h + 1) & mask;
-            c.hs[h] = id;
-        }
+        if (lane == 0) hash_insert(c, id);
         ++c.hs_count;
     } else {
         if (lane == 0) atomicOr(&c.gbm[id >> 5], 1u << (id & 31u));
@@ -190,11 +194,7 @@ __device__ __forceinline__ void mark_many(Common& c, uint32_t lanes, uint32_t w,
     const uint32_t np = __popc(lanes);
     const bool mine = (lanes >> lane) & 1u;
     if (c.hs_count + np <= (1u << c.hs_log2) / 2) {
-        if (mine) {
-            const uint32_t mask = (1u << c.hs_log2) - 1;
-            uint32_t h = hslot(w, c.hs_log2);
-            while (atomicCAS(&c.hs[h], EMPTY, w) != EMPTY) h = (h + 1) & mask;
-        }
+        if (mine) hash_insert(c, w);
         c.hs_count += np;
     } else {
         if (mine) atomicOr(&c.gbm[w >> 5], 1u << (w & 31u));
@@ -1584,7 +1584,8 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
         c.overflow = false;
         c.n_exact = c.n_test = c.n_pass = c.n_visited = c.n_edges = c.n_pes = 0;
         s.reset();
-        for (uint32_t i = lane; i < (1u << c.hs_log2); i += 32) c.hs[i] = EMPTY;
+        for (uint32_t i = lane; i < (1u << c.hs_log2) / 4; i += 32)
+            reinterpret_cast<uint4*>(c.hs)[i] = make_uint4(EMPTY, EMPTY, EMPTY, EMPTY);
 
         // ---- query prep (routing.cpp:253-259): pad, cosine-normalise
         uint32_t status = 0;
