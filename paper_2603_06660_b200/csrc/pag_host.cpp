@@ -567,6 +567,11 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     L.hash_log2 = p.efS <= 200 ? 10 : 8;
     if (const char* e = std::getenv("PAG_GPU_HASH_LOG2")) L.hash_log2 = static_cast<uint32_t>(std::atoi(e));
     L.hash_log2 = std::max(3u, std::min(16u, L.hash_log2));  // >= 2 buckets of 4 slots
+    {
+        uint32_t fill = 50;  // percent of the slots filled before marks spill to the HBM bitmap
+        if (const char* e = std::getenv("PAG_GPU_HASH_FILL")) fill = std::max(1, std::min(90, std::atoi(e)));
+        L.hash_limit = static_cast<uint32_t>((static_cast<uint64_t>(1u << L.hash_log2) * fill) / 100);
+    }
     const uint32_t b = L.b;
     L.rl_cap = L.r_max * b + b;  // every W flush of a query (r_max - 1 end_rounds + the final flush)
     const uint32_t capr = L.rl_cap;

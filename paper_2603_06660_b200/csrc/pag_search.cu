@@ -122,7 +122,7 @@ struct Common {
     // smem table is half full further marks go to this warp's n-bit HBM
     // bitmap (one load per lookup, no probe chains), cleared after the query
     uint32_t* hs;
-    uint32_t hs_log2, hs_count;
+    uint32_t hs_log2, hs_count, hs_limit;  // marks held on chip before the bitmap takes over
     uint32_t* gbm;
     uint32_t gbm_words, gt_count;
     bool gt_used, overflow;
@@ -176,7 +176,7 @@ __device__ __forceinline__ void hash_insert(const Common& c, uint32_t id) {
 
 // warp-uniform call; lane 0 writes
 __device__ __forceinline__ void mark(Common& c, uint32_t id, int lane) {
-    if (c.hs_count < (1u << c.hs_log2) / 2) {
+    if (c.hs_count < c.hs_limit) {
         if (lane == 0) hash_insert(c, id);
         ++c.hs_count;
     } else {
@@ -193,7 +193,7 @@ __device__ __forceinline__ void mark(Common& c, uint32_t id, int lane) {
 __device__ __forceinline__ void mark_many(Common& c, uint32_t lanes, uint32_t w, int lane) {
     const uint32_t np = __popc(lanes);
     const bool mine = (lanes >> lane) & 1u;
-    if (c.hs_count + np <= (1u << c.hs_log2) / 2) {
+    if (c.hs_count + np <= c.hs_limit) {
         if (mine) hash_insert(c, w);
         c.hs_count += np;
     } else {
@@ -1548,6 +1548,7 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
     c.cap_r = P.efS;
     c.hs = reinterpret_cast<uint32_t*>(sw + P.off_hash);
     c.hs_log2 = P.hash_log2;
+    c.hs_limit = P.hash_limit;
     c.gbm = P.gbm + static_cast<uint64_t>(slot) * P.gbm_words;  // zero between queries
     c.gbm_words = P.gbm_words;
     TFB s;
@@ -1600,7 +1601,12 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
             __syncwarp();
         } else {
             const float* qraw = P.queries + static_cast<uint64_t>(qid) * ix.dim;
-            for (uint32_t k = lane; k < ix.dstride; k += 32) c.q[k] = (k < ix.dim) ? __ldg(qraw + k) : 0.0f;
+            if (ix.dim == ix.dstride && (reinterpret_cast<uintptr_t>(qraw) & 15u) == 0) {  // 16-B rows
+                for (uint32_t k = lane; k < ix.dim / 4; k += 32)
+                    reinterpret_cast<float4*>(c.q)[k] = __ldg(reinterpret_cast<const float4*>(qraw) + k);
+            } else {
+                for (uint32_t k = lane; k < ix.dstride; k += 32) c.q[k] = (k < ix.dim) ? __ldg(qraw + k) : 0.0f;
+            }
             __syncwarp();
         }
         if (ix.cosine && !P.qnodes) {
