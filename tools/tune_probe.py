@@ -23,7 +23,7 @@ if os.environ.get("PF_CHILD"):
     ix = pag.load_index(p["index"])
     q = read_fvecs(p["queries"])
     nq = q.shape[0]
-    params = pag.SearchParams(K=K, efS=efs, exact_dist=False)
+    params = pag.SearchParams(K=K, efS=efs, exact_dist=bool(int(os.environ.get("EXACT", "0"))))
     s = torch.cuda.Stream()
     qd = torch.from_numpy(q).cuda()
     outs = [torch.empty((nq, K), dtype=torch.int32, device="cuda"),
