@@ -1506,8 +1506,9 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
         // from the next group/expansion only (in-group duplicates are resolved
         // by `same`), so the inserts are deferred and done in parallel.
         if (passed && !(P.tune & 8u)) mark_many(c, passed, w, lane);
-        const bool not_test = cand && ((same & lt & passed) != 0u);
-        c.n_test += __popc(cand_mask) - __popc(__ballot_sync(FULL, not_test));
+        // a copy skipped after an earlier copy in the group passed is no test
+        c.n_test += __popc(cand_mask);
+        if (any_dup) c.n_test -= __popc(__ballot_sync(FULL, cand && ((same & lt & passed) != 0u)));
         PT(6);
         __syncwarp();
     }
