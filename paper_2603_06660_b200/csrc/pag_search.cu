@@ -615,7 +615,15 @@ struct TfbReg {
 // caches; a change to a slot re-scans only its owner's S slots, all lanes
 // reading consecutive slots (conflict-free). Same selections as the full
 // scans of routing.cpp:32-44,71-80.
-struct TfbMem {
+//
+// WOFF (W in the warp's HBM scratch, L2 latency per access): the caches also
+// carry the winners' aux / id, so the expanded entry and the evicted z_max
+// come from registers; set_visited writes the flag without reading and its
+// owner re-scan is issued at once but folded in only before the next argmin
+// (the loads overlap the expansion); an admission or append touching that
+// owner first folds or supersedes it.
+template <bool WOFF>
+struct TfbMemT {
     Arr W, rf, rt, mi;
     uint32_t b, S;
     uint32_t wsize, rf_head, rf_size, rt_head, rt_size;
@@ -624,6 +632,13 @@ struct TfbMem {
     // this lane's caches over its slots
     uint32_t mn_key, mn_id, mn_slot;  // best unvisited by (sq, id); mn_slot EMPTY if none
     uint32_t mx_key, mx_slot;         // largest sq, lowest slot; mx_slot EMPTY if none
+    // WOFF only
+    uint32_t mn_aux, mx_id, mx_aux;   // aux of the best unvisited, id/aux of the largest
+    uint32_t nx_slot, nx_id, nx_aux;  // warp-uniform: the entry next_unvisited returned
+    float nx_sq;
+    uint32_t zmax_id, zmax_aux;       // warp-uniform
+    uint32_t pend_o;                  // owner whose re-scan is in flight (EMPTY: none)
+    uint32_t pk, pid, pax;            // its slot o*S + lane as loaded
 
     __device__ void init(uint32_t b_, uint8_t* sw, uint8_t* gw, const SearchLaunch& P) {
         b = b_;
@@ -637,6 +652,11 @@ struct TfbMem {
         mn_key = mn_id = 0xffffffffu;
         mn_slot = mx_slot = EMPTY;
         mx_key = 0;
+        if (WOFF) {
+            mn_aux = mx_id = mx_aux = 0;
+            nx_slot = EMPTY;
+            pend_o = EMPTY;
+        }
     }
     __device__ void reset() {
         wsize = rf_head = rf_size = rt_head = rt_size = 0;
@@ -647,39 +667,90 @@ struct TfbMem {
     __device__ float admission_sq() const { return wsize < b ? CUDART_INF_F : zmax_sq; }
     __device__ float admission_dist() const { return wsize < b ? CUDART_INF_F : zmax_dist; }
 
-    // re-derive owner o's caches from its slots (warp-cooperative)
-    __device__ void rescan(uint32_t o, int lane) {
-        uint32_t nk = 0xffffffffu, ni = 0xffffffffu, ns = EMPTY, xk = 0, xs = EMPTY;
-        for (uint32_t j = lane; j < S; j += 32) {
-            const uint32_t i = o * S + j;
-            if (i >= wsize) break;
-            const uint32_t k = fkey(W.sq[i]);
-            if (xs == EMPTY || k > xk) {
-                xk = k;
-                xs = i;
-            }
-            if (!(W.aux[i] & VISITED)) {
-                const uint32_t id = W.id[i];
-                if (ns == EMPTY || k < nk || (k == nk && id < ni)) {
-                    nk = k;
-                    ni = id;
-                    ns = i;
-                }
-            }
-        }
+    // owner o's caches from per-lane candidates (one set of warp reductions);
+    // W ids are distinct, so (key, id) names one slot, whose lane supplies
+    // slot and aux; the max is the lowest slot among equal keys
+    __device__ void fold(uint32_t o, uint32_t nk, uint32_t ni, uint32_t ns, uint32_t na, uint32_t xk, uint32_t xs,
+                         uint32_t xi, uint32_t xa, int lane) {
         const uint32_t m1 = __reduce_min_sync(FULL, ns == EMPTY ? 0xffffffffu : nk);
         const bool c1 = ns != EMPTY && nk == m1;
         const uint32_t m2 = __reduce_min_sync(FULL, c1 ? ni : 0xffffffffu);
-        const uint32_t s1 = __reduce_min_sync(FULL, (c1 && ni == m2) ? ns : EMPTY);
         const uint32_t x1 = __reduce_max_sync(FULL, xs == EMPTY ? 0u : xk);
         const uint32_t xs1 = __reduce_min_sync(FULL, (xs != EMPTY && xk == x1) ? xs : EMPTY);
+        uint32_t s1, a1 = 0, xi1 = 0, xa1 = 0;
+        if (WOFF) {
+            const uint32_t wm = __ballot_sync(FULL, c1 && ni == m2);
+            const int lm = wm ? __ffs(wm) - 1 : 0;
+            s1 = wm ? __shfl_sync(FULL, ns, lm) : EMPTY;
+            a1 = __shfl_sync(FULL, na, lm);
+            const uint32_t wx = __ballot_sync(FULL, xs != EMPTY && xs == xs1);
+            const int lx = wx ? __ffs(wx) - 1 : 0;
+            xi1 = __shfl_sync(FULL, xi, lx);
+            xa1 = __shfl_sync(FULL, xa, lx);
+        } else {
+            s1 = __reduce_min_sync(FULL, (c1 && ni == m2) ? ns : EMPTY);
+        }
         if (static_cast<uint32_t>(lane) == o) {
             mn_key = m1;
             mn_id = m2;
             mn_slot = s1;
             mx_key = x1;
             mx_slot = xs1;
+            if (WOFF) {
+                mn_aux = a1;
+                mx_id = xi1;
+                mx_aux = xa1;
+            }
         }
+    }
+    // re-derive owner o's caches from its slots (warp-cooperative)
+    __device__ void rescan(uint32_t o, int lane) {
+        if (WOFF && pend_o == o) pend_o = EMPTY;  // superseded
+        uint32_t nk = 0xffffffffu, ni = 0xffffffffu, ns = EMPTY, na = 0, xk = 0, xs = EMPTY, xi = 0, xa = 0;
+        for (uint32_t j = lane; j < S; j += 32) {
+            const uint32_t i = o * S + j;
+            if (i >= wsize) break;
+            const uint32_t k = fkey(W.sq[i]);
+            const uint32_t a = W.aux[i];
+            const uint32_t id = WOFF ? W.id[i] : 0u;
+            if (xs == EMPTY || k > xk) {
+                xk = k;
+                xs = i;
+                xi = id;
+                xa = a;
+            }
+            if (!(a & VISITED)) {
+                const uint32_t idn = WOFF ? id : W.id[i];
+                if (ns == EMPTY || k < nk || (k == nk && idn < ni)) {
+                    nk = k;
+                    ni = idn;
+                    ns = i;
+                    na = a;
+                }
+            }
+        }
+        fold(o, nk, ni, ns, na, xk, xs, xi, xa, lane);
+    }
+    // WOFF: fold the in-flight re-scan of pend_o (S <= 32: one slot per lane)
+    __device__ void fold_pending(int lane) {
+        if (!WOFF || pend_o == EMPTY) return;
+        const uint32_t o = pend_o;
+        pend_o = EMPTY;
+        uint32_t nk = 0xffffffffu, ni = 0xffffffffu, ns = EMPTY, na = 0, xk = 0, xs = EMPTY, xi = 0, xa = 0;
+        const uint32_t i = o * S + static_cast<uint32_t>(lane);
+        if (static_cast<uint32_t>(lane) < S && i < wsize) {
+            xk = pk;
+            xs = i;
+            xi = pid;
+            xa = pax;
+            if (!(pax & VISITED)) {
+                nk = pk;
+                ni = pid;
+                ns = i;
+                na = pax;
+            }
+        }
+        fold(o, nk, ni, ns, na, xk, xs, xi, xa, lane);
     }
     // routing.cpp:32-44 from the caches: argmax, first slot on ties
     __device__ void zmax_from_caches() {
@@ -687,6 +758,12 @@ struct TfbMem {
         zmax_sq = __uint_as_float(m);  // the key is the value (sq >= 0: x + 0 == x)
         zmax_dist = __fsqrt_rn(zmax_sq);
         zmax_idx = __reduce_min_sync(FULL, (mx_slot != EMPTY && mx_key == m) ? mx_slot : EMPTY);
+        if (WOFF) {
+            const uint32_t wz = __ballot_sync(FULL, mx_slot != EMPTY && mx_slot == zmax_idx);
+            const int lz = wz ? __ffs(wz) - 1 : 0;
+            zmax_id = __shfl_sync(FULL, mx_id, lz);
+            zmax_aux = __shfl_sync(FULL, mx_aux, lz);
+        }
     }
     __device__ void recompute_zmax(int lane) {  // after a wholesale refill of W
         clear_caches();
@@ -700,20 +777,49 @@ struct TfbMem {
         zmax_from_caches();
     }
     // routing.cpp:71-80: argmin over unvisited by (sq, id)
-    __device__ uint32_t next_unvisited(int) const {
+    __device__ uint32_t next_unvisited(int lane) {
+        fold_pending(lane);
         if (!__ballot_sync(FULL, mn_slot != EMPTY)) return EMPTY;
         const uint32_t m1 = __reduce_min_sync(FULL, mn_slot == EMPTY ? 0xffffffffu : mn_key);
         const bool c1 = mn_slot != EMPTY && mn_key == m1;
         const uint32_t m2 = __reduce_min_sync(FULL, c1 ? mn_id : 0xffffffffu);
-        return __reduce_min_sync(FULL, (c1 && mn_id == m2) ? mn_slot : EMPTY);
+        if (!WOFF) return __reduce_min_sync(FULL, (c1 && mn_id == m2) ? mn_slot : EMPTY);
+        const int l = __ffs(__ballot_sync(FULL, c1 && mn_id == m2)) - 1;  // distinct ids: one owner
+        nx_slot = __shfl_sync(FULL, mn_slot, l);
+        nx_aux = __shfl_sync(FULL, mn_aux, l);
+        nx_id = m2;
+        nx_sq = __uint_as_float(m1);  // the key is the value (sq >= 0)
+        return nx_slot;
     }
     __device__ void entry(uint32_t slot, uint32_t& id, float& sq, uint32_t& deg) const {
+        if (WOFF && slot == nx_slot) {
+            id = nx_id;
+            sq = nx_sq;
+            deg = nx_aux & ~VISITED;
+            return;
+        }
         id = W.id[slot];
         sq = W.sq[slot];
         deg = W.aux[slot] & ~VISITED;
     }
     __device__ uint32_t entry_id(uint32_t slot) const { return W.id[slot]; }
     __device__ void set_visited(uint32_t slot, int lane) {
+        if (WOFF && slot == nx_slot && S <= 32) {
+            // no read: the flag is stored, the owner's slots are requested now
+            // and folded in before the next argmin (fold_pending)
+            const uint32_t o = slot / S;
+            if (lane == 0) W.aux[slot] = nx_aux | VISITED;
+            nx_slot = EMPTY;
+            const uint32_t i = o * S + static_cast<uint32_t>(lane);
+            if (static_cast<uint32_t>(lane) < S && i < wsize) {
+                pk = fkey(W.sq[i]);
+                pid = W.id[i];
+                pax = (i == slot) ? (nx_aux | VISITED) : W.aux[i];
+            }
+            pend_o = o;
+            __syncwarp();
+            return;
+        }
         const uint32_t a = W.aux[slot];
         __syncwarp();
         if (lane == 0) W.aux[slot] = a | VISITED;
@@ -722,6 +828,7 @@ struct TfbMem {
     }
     __device__ void append(uint32_t id, float sq, uint32_t deg, int lane) {
         const uint32_t slot = wsize;
+        if (WOFF && pend_o == slot / S) fold_pending(lane);
         if (lane == 0) {
             W.id[slot] = id;
             W.sq[slot] = sq;
@@ -733,10 +840,15 @@ struct TfbMem {
                 mn_key = k;
                 mn_id = id;
                 mn_slot = slot;
+                if (WOFF) mn_aux = deg;
             }
             if (mx_slot == EMPTY || k > mx_key) {
                 mx_key = k;
                 mx_slot = slot;
+                if (WOFF) {
+                    mx_id = id;
+                    mx_aux = deg;
+                }
             }
         }
         ++wsize;
@@ -744,6 +856,10 @@ struct TfbMem {
             zmax_idx = wsize - 1;
             zmax_sq = sq;
             zmax_dist = __fsqrt_rn(sq);
+            if (WOFF) {
+                zmax_id = id;
+                zmax_aux = deg;
+            }
         }
         __syncwarp();
     }
@@ -790,11 +906,15 @@ struct TfbMem {
             return;
         }
         const uint32_t z = zmax_idx;
-        const uint32_t oid = W.id[z];
-        const float osq = W.sq[z];
-        const uint32_t oaux = W.aux[z] & ~VISITED;
-        __syncwarp();
-        ring_push(rt, b, rt_head, rt_size, oid, osq, oaux, lane);
+        if (WOFF) {
+            ring_push(rt, b, rt_head, rt_size, zmax_id, zmax_sq, zmax_aux & ~VISITED, lane);
+        } else {
+            const uint32_t oid = W.id[z];
+            const float osq = W.sq[z];
+            const uint32_t oaux = W.aux[z] & ~VISITED;
+            __syncwarp();
+            ring_push(rt, b, rt_head, rt_size, oid, osq, oaux, lane);
+        }
         if (lane == 0) {
             W.id[z] = id;
             W.sq[z] = sq;
@@ -1832,8 +1952,11 @@ cudaError_t dispatch_tfb(const SearchLaunch& L, int grid, cudaStream_t stream, i
     if (L.b <= 32)
         return L.exact_dist ? dispatch_nch<TfbReg, true>(L, grid, smem, stream, bps)
                             : dispatch_nch<TfbReg, false>(L, grid, smem, stream, bps);
-    return L.exact_dist ? dispatch_nch<TfbMem, true>(L, grid, smem, stream, bps)
-                        : dispatch_nch<TfbMem, false>(L, grid, smem, stream, bps);
+    if (!L.W_in_smem)
+        return L.exact_dist ? dispatch_nch<TfbMemT<true>, true>(L, grid, smem, stream, bps)
+                            : dispatch_nch<TfbMemT<true>, false>(L, grid, smem, stream, bps);
+    return L.exact_dist ? dispatch_nch<TfbMemT<false>, true>(L, grid, smem, stream, bps)
+                        : dispatch_nch<TfbMemT<false>, false>(L, grid, smem, stream, bps);
 }
 
 }  // namespace
