@@ -776,6 +776,8 @@ void search_on_replica(pag_gpu_index& ix, Replica& r, const pag_search_params& p
         ca.pes_n = reinterpret_cast<uint32_t*>(r.d_out + 2 * ob_ids + ob_n + ob_st + ob_list + ob_pes);
     }
     const ConstructionArgs* cap = ch ? &ca : nullptr;
+    // entries past each pes list are zero (the kernel writes min(n, cap))
+    if (ch && ob_pes) cuda_check(cudaMemsetAsync(ca.pes, 0, ob_pes, r.stream), "memset pes");
     // queries in pinned (mapped) host memory are read by the kernel in place
     // over PCIe at each query's start (3 KB per query at d=768), which
     // overlaps the transfer with the search; pageable ones are copied first
@@ -834,9 +836,6 @@ void search_on_replica(pag_gpu_index& ix, Replica& r, const pag_search_params& p
         cuda_check(cudaMemcpyAsync(ch->pes_n, ca.pes_n, ob_pn, cudaMemcpyDeviceToHost, r.stream), "D2H pes_n");
     }
     cuda_check(cudaStreamSynchronize(r.stream), "D2H");
-    if (ch && ch->pes_cap)  // entries past each list are unspecified on the device: zero them
-        for (uint64_t i = 0; i < nq; ++i)
-            for (uint32_t j = std::min(ch->pes_n[i], ch->pes_cap); j < ch->pes_cap; ++j) ch->pes[i * ch->pes_cap + j] = 0;
     uint32_t so = 0;
     for (uint64_t i = 0; i < nq; ++i) {
         const uint32_t* s = &st[i * pagdev::kStatWords];

@@ -208,19 +208,28 @@ class PagIndex:
         return PendingBatch(self, int(t.value), q, res)
 
     def construction_search(self, nodes, params: Optional[SearchParams] = None,
-                            collect_pes: Optional[bool] = None, pes_cap: int = 256) -> ConstructionResult:
+                            collect_pes: Optional[bool] = None, pes_cap: int = 256,
+                            out: Optional[ConstructionResult] = None) -> ConstructionResult:
         """The search step of insert_with_state (builder.cpp:218-227) for
         nodes already in the index: query = the node's stored row, K = efS =
         efC, b = b_build, PES tracking per enable_pes (params / collect_pes
-        override). Returns results, counters and pes_rejected lists."""
+        override). Returns results, counters and pes_rejected lists; `out`
+        (same shapes, C-contiguous) is filled instead of new arrays."""
         nodes = np.ascontiguousarray(nodes, np.uint32).reshape(-1)
         nn = len(nodes)
         K = int(params.K) if params is not None else self.efC
-        ids = np.zeros((nn, K), np.uint32)
-        sq = np.zeros((nn, K), np.float32)
-        n_out = np.zeros(nn, np.uint32)
-        pes = np.zeros((nn, pes_cap), np.uint32)
-        pes_n = np.zeros(nn, np.uint32)
+        if out is not None:
+            ids, sq, n_out, pes, pes_n = out.ids, out.sq, out.n_out, out.pes, out.pes_n
+            for a, shape, dt in ((ids, (nn, K), np.uint32), (sq, (nn, K), np.float32), (n_out, (nn,), np.uint32),
+                                 (pes, (nn, pes_cap), np.uint32), (pes_n, (nn,), np.uint32)):
+                if a.shape != shape or a.dtype != dt or not a.flags.c_contiguous:
+                    raise ValueError("out arrays do not match the batch")
+        else:
+            ids = np.zeros((nn, K), np.uint32)
+            sq = np.zeros((nn, K), np.float32)
+            n_out = np.zeros(nn, np.uint32)
+            pes = np.zeros((nn, pes_cap), np.uint32)
+            pes_n = np.zeros(nn, np.uint32)
         st = (SearchStatsC * max(nn, 1))()
         pc = params.to_c() if params is not None else None
         cp = -1 if collect_pes is None else int(bool(collect_pes))
@@ -231,8 +240,11 @@ class PagIndex:
                                               n_out.ctypes.data if nn else None, st,
                                               pes.ctypes.data if pes_cap and nn else None, pes_cap,
                                               pes_n.ctypes.data if nn else None))
-        stats = np.ctypeslib.as_array(C.cast(st, C.POINTER(C.c_uint64)), (max(nn, 1), 5))[:nn].copy()
-        return ConstructionResult(ids, sq, n_out, stats, pes, pes_n)
+        stats = np.ctypeslib.as_array(C.cast(st, C.POINTER(C.c_uint64)), (max(nn, 1), 5))[:nn]
+        if out is not None:
+            out.stats[:] = stats
+            return out
+        return ConstructionResult(ids, sq, n_out, stats.copy(), pes, pes_n)
 
     def construction_search_device(self, nodes_ptr: int, nn: int, params: Optional[SearchParams],
                                    collect_pes: Optional[bool], ids_ptr: int, sq_ptr: int, n_out_ptr: int,

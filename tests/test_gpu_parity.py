@@ -446,3 +446,25 @@ def test_duplicate_targets_in_group_bitexact(pag, built, tmp_path):
             assert_same_results((got.ids, got.sq, got.n_out, got.stats), want, f"duplicates {K}/{efS}")
     finally:
         ix.close()
+
+
+def test_construction_search_reuses_out_arrays(pag, built):
+    """construction_search(out=...) fills caller arrays (stale contents are
+    overwritten, entries past each pes list are zero) and equals a fresh call."""
+    fx = built("deg64")
+    ix = gpu_index(pag, fx["index"])
+    nodes = np.arange(3, ix.n, 13, dtype=np.uint32)
+    fresh = ix.construction_search(nodes)
+    nn, K, cap = len(nodes), ix.efC, 256
+    out = pag.ConstructionResult(np.full((nn, K), 7, np.uint32), np.full((nn, K), 7, np.float32),
+                                 np.full(nn, 7, np.uint32), np.zeros((nn, 5), np.uint64),
+                                 np.full((nn, cap), 7, np.uint32), np.full(nn, 7, np.uint32))
+    got = ix.construction_search(nodes, out=out)
+    assert got is out
+    for a, b in ((got.ids, fresh.ids), (got.sq, fresh.sq), (got.n_out, fresh.n_out), (got.stats, fresh.stats),
+                 (got.pes, fresh.pes), (got.pes_n, fresh.pes_n)):
+        assert np.array_equal(a, b)
+    for i in range(nn):
+        assert not got.pes[i, min(int(got.pes_n[i]), cap):].any()
+    with pytest.raises(ValueError):
+        ix.construction_search(nodes[:-1], out=out)
