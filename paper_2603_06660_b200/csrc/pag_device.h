@@ -102,10 +102,10 @@ struct SearchLaunch {
     uint32_t off_rl, rl_in_smem, rl_cap;  // R_L append buffer (+ sort scratch)
     uint32_t off_merge, merge_in_smem;
     uint32_t warps_per_block;
-    // experiment bits (PAG_GPU_TUNE): 8 sequential marks (diagnostic), 64
-    // row-pair reference-order distances. (Adjacency prefetch at admission
-    // or of the predicted next node, bulk or per-lane, measured slower on
-    // cfg2/cfg3/cfg4 and was removed.)
+    // experiment bits (PAG_GPU_TUNE, A/B runs in tools/tune_probe.py); no
+    // production path reads them. Measured and removed: adjacency look-ahead
+    // into smem by cp.async.bulk, TMEM-resident W, row-pair and 8-row
+    // reference-order distances
     uint32_t tune;
 };
 

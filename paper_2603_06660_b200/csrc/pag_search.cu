@@ -1212,69 +1212,6 @@ __device__ void dist_fast_pairs(const SearchLaunch& P, Common& c, uint32_t items
     }
 }
 
-// Reference-order distances two rows at a time: the half-warp of a row loads
-// it whole (all 2*NCH float4 per lane in flight), then for each 64-float
-// slice the squared differences are scattered transposed into smem and lanes
-// 0..3 of the half run accumulator chains c = 0..3 over it in k order.
-// Element k = 64 i + 4 hl + c sits in slice i, lane hl, component c, so chain
-// c visits slices in order and lanes 0..15 within a slice: exactly the
-// reference's sequence k = c, c + 4, c + 8, ... (padded_dim = 128 NCH: no tail).
-template <int NCH>
-__device__ void dist_exact_pairs(const SearchLaunch& P, Common& c, uint32_t items, uint32_t w, int lane) {
-    constexpr int NL = 2 * NCH;
-    constexpr int PSTR = 20;  // floats per (row, chain) slice row: 16 + pad, 16-B aligned
-    const IndexView& ix = P.ix;
-    const uint32_t DS = 128u * NCH;
-    const int half = lane >> 4, hl = lane & 15;
-    uint32_t rest = items;
-    while (rest) {
-        const int j0 = __ffs(rest) - 1;
-        rest &= rest - 1;
-        int j1 = j0;
-        bool two = false;
-        if (rest) {
-            j1 = __ffs(rest) - 1;
-            rest &= rest - 1;
-            two = true;
-        }
-        const int jm = half ? j1 : j0;
-        const uint32_t wr = __shfl_sync(FULL, w, jm);
-        const float* rp = ix.rows + static_cast<uint64_t>(wr) * DS + 4u * hl;
-        float4 v[NL];
-#pragma unroll
-        for (int i = 0; i < NL; ++i) v[i] = ldg_f4(rp + 64 * i);
-        float acc = 0.0f;
-        float* st = c.stage + (half * 4) * PSTR + hl;
-        const float* cs = c.stage + (half * 4 + hl) * PSTR;  // chain lanes hl < 4
-#pragma unroll
-        for (int i = 0; i < NL; ++i) {
-            const float4 qv = *reinterpret_cast<const float4*>(c.q + 64 * i + 4 * hl);
-            const float2 lo = sq2(make_float2(v[i].x, v[i].y), make_float2(qv.x, qv.y));
-            const float2 hi = sq2(make_float2(v[i].z, v[i].w), make_float2(qv.z, qv.w));
-            st[0] = lo.x;
-            st[PSTR] = lo.y;
-            st[2 * PSTR] = hi.x;
-            st[3 * PSTR] = hi.y;
-            __syncwarp();
-            if (hl < 4) {
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const float4 x = *reinterpret_cast<const float4*>(cs + 4 * t);
-                    acc = __fadd_rn(acc, x.x);
-                    acc = __fadd_rn(acc, x.y);
-                    acc = __fadd_rn(acc, x.z);
-                    acc = __fadd_rn(acc, x.w);
-                }
-            }
-            __syncwarp();
-        }
-        const float a1 = __shfl_down_sync(FULL, acc, 1);
-        const float a2 = __shfl_down_sync(FULL, acc, 2);
-        const float a3 = __shfl_down_sync(FULL, acc, 3);
-        if (hl == 0 && (half == 0 || two)) c.sqbuf[jm] = __fadd_rn(__fadd_rn(acc, a1), __fadd_rn(a2, a3));
-    }
-}
-
 template <int NCH>
 __device__ void dist_fast(const SearchLaunch& P, Common& c, uint32_t items, uint32_t w, int lane) {
     const IndexView& ix = P.ix;
@@ -1355,9 +1292,7 @@ __device__ __forceinline__ void distances(const SearchLaunch& P, Common& c, uint
     }
     if (EXACT) {
         if constexpr (NCH > 0 && NCH <= 6) {
-            if (P.tune & 64u)  // row-pair variant (measured slower: serial chains per pair)
-                dist_exact_pairs<NCH>(P, c, items, w, lane);
-            else if constexpr (NCH >= 2)
+            if constexpr (NCH >= 2)
                 dist_exact_la2<(NCH >= 2 ? NCH : 2)>(P, c, items, w, lane);
             else
                 dist_exact<NCH>(P, c, items, w, lane);
@@ -1551,7 +1486,7 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
         // order (the radius cannot change before it), that one is admitted
         // (the radius shrinks) and the rest are re-tested
         uint32_t passed = 0;
-        if (!any_dup && !(P.tune & 8u)) {
+        if (!any_dup) {
             const float sqv = spec ? c.sqbuf[lane] : 0.0f;
             const uint32_t dgv = spec ? c.degbuf[lane] : 0u;
             uint32_t rem = surv;
@@ -1585,7 +1520,7 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
             c.n_pass += __popc(passed);
             c.n_exact += __popc(passed);
         }
-        uint32_t rem = (!any_dup && !(P.tune & 8u)) ? 0u : surv;  // sequential replay (duplicates, diagnostics)
+        uint32_t rem = any_dup ? surv : 0u;  // sequential replay (in-group duplicates)
         while (rem) {
             const int jl = __ffs(rem) - 1;
             rem &= rem - 1;
@@ -1615,7 +1550,6 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
             ++c.n_exact;
             const float sq_j = c.sqbuf[jl];
             const uint32_t deg_j = c.degbuf[jl];
-            if (P.tune & 8u) mark(c, w_j, lane);  // (diagnostic) sequential marking
             if (sq_j < s.admission_sq()) {
                 s.admit(w_j, sq_j, deg_j, lane);
             } else {
@@ -1625,7 +1559,7 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
         // marks of this group's passes (routing.cpp:183). Later lookups come
         // from the next group/expansion only (in-group duplicates are resolved
         // by `same`), so the inserts are deferred and done in parallel.
-        if (passed && !(P.tune & 8u)) mark_many(c, passed, w, lane);
+        if (passed) mark_many(c, passed, w, lane);
         // a copy skipped after an earlier copy in the group passed is no test
         c.n_test += __popc(cand_mask);
         if (any_dup) c.n_test -= __popc(__ballot_sync(FULL, cand && ((same & lt & passed) != 0u)));
