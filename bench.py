@@ -462,9 +462,10 @@ def run_pag(args, cfg, paths, rank, world, local_rank, threads, dist):
     for _ in range(e2e_steps):
         ix.search_batch(qh, params)
     sync_s = max_over_ranks(max(time.perf_counter() - t, 1e-9), dist, dev)
-    # the same through the asynchronous API, up to 3 batches in flight: the
-    # kernel reads each step's pinned queries in place and writes its results
-    # into pinned host memory; wait() unpacks them into the step's arrays
+    # the same through the asynchronous API, up to 4 batches in flight (the
+    # library's ring depth), all K steps: the kernel reads each step's pinned
+    # queries in place and writes its results into pinned host memory; wait()
+    # unpacks them into the step's arrays
     if dist is not None:
         dist.barrier()
     outs = [pag.BatchResult(np.zeros((nq, K), np.uint32), np.zeros((nq, K), np.float32), np.zeros(nq, np.uint32),
@@ -473,16 +474,17 @@ def run_pag(args, cfg, paths, rank, world, local_rank, threads, dist):
         ix.search_submit(qh, params, out=outs[i]).wait()
     if dist is not None:
         dist.barrier()
+    a_steps = 0 if args.no_e2e else max(3, args.steps)
     t = time.perf_counter()
     pending = []
-    for i in range(e2e_steps):
+    for i in range(a_steps):
         pending.append(ix.search_submit(qh, params, out=outs[i % 4]))
-        if len(pending) == 3:
+        if len(pending) == 4:
             pending.pop(0).wait()
     while pending:
         pending.pop(0).wait()
     e2e_s = max_over_ranks(max(time.perf_counter() - t, 1e-9), dist, dev)
-    e2e_qps = world * nq * e2e_steps / e2e_s
+    e2e_qps = world * nq * a_steps / e2e_s
     h2d = nq * queries.shape[1] * 4
     d2h = nq * K * 8 + nq * 4 + nq * 8 * 4
 
@@ -532,7 +534,7 @@ def run_pag(args, cfg, paths, rank, world, local_rank, threads, dist):
                    "parallelism": f"query shards, index replica per GPU x{world}"},
         "e2e": {"value": round(e2e_qps, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "path": "pag_gpu_search_submit/wait from pinned host queries, up to 3 batches in flight "
+                "path": f"pag_gpu_search_submit/wait from pinned host queries, {a_steps} steps, up to 4 batches in flight "
                         "(queries read in place over PCIe, results written to pinned host memory, "
                         "unpacked into 4 rotating preallocated result arrays)",
                 "sync_value": round(world * nq * e2e_steps / sync_s, 1),
