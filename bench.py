@@ -165,11 +165,28 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def cpu_reference(index_path: str, queries_path: str, K: int, efS: int, threads: int, limit: int, reps: int):
-    out = subprocess.run([REF_BIN, "search", f"--index={index_path}", f"--queries={queries_path}",
-                          f"--K={K}", f"--efS={efS}", f"--threads={threads}", f"--limit={limit}",
-                          f"--reps={reps}"], check=True, capture_output=True, text=True)
+def cpu_reference(index_path: str, queries_path: str, K: int, efS: int, threads: int, limit: int, reps: int,
+                  out_path: str = None):
+    """The reference's own search (oracle/_ref/pag_ref) timed on the host cores;
+    with out_path its results are written there (the checker of the full-size
+    parity line: read_reference_results)."""
+    cmd = [REF_BIN, "search", f"--index={index_path}", f"--queries={queries_path}", f"--K={K}", f"--efS={efS}",
+           f"--threads={threads}", f"--limit={limit}", f"--reps={reps}"]
+    if out_path:
+        cmd.append(f"--out={out_path}")
+    out = subprocess.run(cmd, check=True, capture_output=True, text=True)
     return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def read_reference_results(path: str):
+    """pag_ref search --out: u64 nq, u64 K, ids u32[nq K], sq f32[nq K], n_out u32[nq], counters u64[nq 4]."""
+    with open(path, "rb") as f:
+        nq, k = (int(x) for x in np.frombuffer(f.read(16), np.uint64))
+        ids = np.frombuffer(f.read(nq * k * 4), np.uint32).reshape(nq, k)
+        sq = np.frombuffer(f.read(nq * k * 4), np.float32).reshape(nq, k)
+        n_out = np.frombuffer(f.read(nq * 4), np.uint32)
+        st = np.frombuffer(f.read(nq * 32), np.uint64).reshape(nq, 4)
+    return ids, sq, n_out, st
 
 
 def cpu_model():
@@ -427,6 +444,7 @@ def run_pag(args, cfg, paths, rank, world, local_rank, threads, dist):
     ids_o = ids_dev.cpu().numpy().view(np.uint32)
     sq_o = sq_dev.cpu().numpy()
     n_o = n_dev.cpu().numpy().view(np.uint32)
+    st_o = st_dev.cpu().numpy().view(np.uint32)
     same_set = np.mean([set(ids_main[i, :n_main[i]].tolist()) == set(ids_o[i, :n_o[i]].tolist())
                         for i in range(nq)])
     common = (ids_main == ids_o) & (np.arange(K)[None, :] < np.minimum(n_main, n_o)[:, None])
@@ -503,12 +521,33 @@ def run_pag(args, cfg, paths, rank, world, local_rank, threads, dist):
         traffic = None
     # cpu baseline (reference search, all host cores, bounded sample)
     cpu = None
+    parity = None
     if world == 1 and not args.no_cpu_baseline and os.path.exists(REF_BIN):
         lim = min(nq, 4000)
-        c = cpu_reference(paths["index"], paths["queries"], K, efs, threads, lim, 3)
+        ref_out = os.path.join(os.path.dirname(paths["index"]), "ref_results.bin")
+        c = cpu_reference(paths["index"], paths["queries"], K, efs, threads, lim, 3, out_path=ref_out)
         cpu = {"value": round(c["qps"], 1), "unit": "queries/s", "cores": threads, "kind": "reference",
                "sample": f"first {lim} queries x 3 timed sweeps after 1 warm sweep, "
                          f"reference search (oracle/_ref/pag_ref, g++ -O3), {threads} threads on {cpu_model()}"}
+        # full-size parity against the reference's own results on those queries
+        r_ids, r_sq, r_n, r_st = read_reference_results(ref_out)
+        by_mode = {args.dist: (ids_main, sq_main, n_main, stats), other_mode: (ids_o, sq_o, n_o, st_o)}
+        parity = {"queries": lim, "checker": "pag_ref search --out (the reference built from its own sources)"}
+        for mode, (g_ids, g_sq, g_n, g_st) in by_mode.items():
+            g_ids, g_sq, g_n = g_ids[:lim], g_sq[:lim], g_n[:lim]
+            cnt = (g_st[:lim, :4].astype(np.uint64) == r_st).all(axis=1)
+            same_ids = np.array([np.array_equal(g_ids[i, :g_n[i]], r_ids[i, :r_n[i]]) for i in range(lim)])
+            same_sq = np.array([np.array_equal(g_sq[i, :g_n[i]].view(np.uint32), r_sq[i, :r_n[i]].view(np.uint32))
+                                for i in range(lim)])
+            sets = np.array([set(g_ids[i, :g_n[i]].tolist()) == set(r_ids[i, :r_n[i]].tolist()) for i in range(lim)])
+            common = (g_ids == r_ids) & (np.arange(K)[None, :] < np.minimum(g_n, r_n)[:, None])
+            rel = np.abs(g_sq - r_sq) / np.maximum(np.abs(r_sq), 1e-30)
+            parity[mode] = {"ids_equal": round(float(same_ids.mean()), 5), "sq_bit_equal": round(float(same_sq.mean()), 5),
+                            "counters_equal": round(float(cnt.mean()), 5),
+                            "id_sets_equal": round(float(sets.mean()), 5),
+                            "max_rel_sq_diff": float(rel[common].max()) if common.any() else 0.0,
+                            "recall_delta": round(pag.mean_recall(g_ids, g_n, gt_ids[:lim], gt_sq[:lim], K)
+                                                  - pag.mean_recall(r_ids, r_n, gt_ids[:lim], gt_sq[:lim], K), 5)}
     sm = stats.astype(np.float64)
     line = {
         "metric": f"QPS at recall@{K}={args.target_recall} (batched search, {cfg['n']}x{cfg['d']})",
@@ -550,6 +589,7 @@ def run_pag(args, cfg, paths, rank, world, local_rank, threads, dist):
         "status_bits": status,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
+        "reference_parity": parity,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
