@@ -647,11 +647,26 @@ def cons_nodes(n: int, count: int, offset: int = 0) -> np.ndarray:
     return ((np.arange(count, dtype=np.uint64) * CONS_STRIDE + offset) % n).astype(np.uint32)
 
 
-def cpu_construction(index_path: str, threads: int, count: int, reps: int):
-    out = subprocess.run([REF_BIN, "build-search", f"--index={index_path}", f"--count={count}",
-                          f"--stride={CONS_STRIDE}", f"--threads={threads}", f"--reps={reps}"],
-                         check=True, capture_output=True, text=True)
+def cpu_construction(index_path: str, threads: int, count: int, reps: int, out_path: str = None):
+    cmd = [REF_BIN, "build-search", f"--index={index_path}", f"--count={count}", f"--stride={CONS_STRIDE}",
+           f"--threads={threads}", f"--reps={reps}"]
+    if out_path:
+        cmd.append(f"--out={out_path}")
+    out = subprocess.run(cmd, check=True, capture_output=True, text=True)
     return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def read_reference_construction(path: str):
+    """pag_ref build-search --out: u64 nn, K, cap; ids; sq; n_out; counters u64[nn 4]; pes_n; pes[nn cap]."""
+    with open(path, "rb") as f:
+        nn, k, cap = (int(x) for x in np.frombuffer(f.read(24), np.uint64))
+        ids = np.frombuffer(f.read(nn * k * 4), np.uint32).reshape(nn, k)
+        sq = np.frombuffer(f.read(nn * k * 4), np.float32).reshape(nn, k)
+        n_out = np.frombuffer(f.read(nn * 4), np.uint32)
+        st = np.frombuffer(f.read(nn * 32), np.uint64).reshape(nn, 4)
+        pes_n = np.frombuffer(f.read(nn * 4), np.uint32)
+        pes = np.frombuffer(f.read(nn * cap * 4), np.uint32).reshape(nn, cap)
+    return ids, sq, n_out, st, pes_n, pes
 
 
 def run_construction(args, cfg, paths, rank, world, local_rank, threads, dist):
@@ -702,7 +717,8 @@ def run_construction(args, cfg, paths, rank, world, local_rank, threads, dist):
         ms = max_over_ranks(ev[0].elapsed_time(ev[1]), dist, dev)
         st = bufs[3].cpu().numpy().view(np.uint32).astype(np.uint64)
         modes[mode] = {"ms": ms, "steps": steps, "stats": st, "ids": bufs[0].cpu().numpy().view(np.uint32).copy(),
-                       "n": bufs[2].cpu().numpy().view(np.uint32).copy(),
+                       "sq": bufs[1].cpu().numpy().copy(), "n": bufs[2].cpu().numpy().view(np.uint32).copy(),
+                       "pes": bufs[4].cpu().numpy().view(np.uint32).copy(),
                        "pes_n": bufs[5].cpu().numpy().view(np.uint32).copy()}
     m = modes["exact"]
     value = world * nn * m["steps"] / (m["ms"] / 1e3)
@@ -731,14 +747,30 @@ def run_construction(args, cfg, paths, rank, world, local_rank, threads, dist):
             dist.destroy_process_group()
         return
     cpu = None
+    parity = None
     if world == 1 and not args.no_cpu_baseline and os.path.exists(REF_BIN):
         lim = min(nn, 2000)
-        c = cpu_construction(paths["index"], threads, lim, 2)
+        ref_out = os.path.join(os.path.dirname(paths["index"]), "ref_construction.bin")
+        c = cpu_construction(paths["index"], threads, lim, 2, out_path=ref_out)
         cpu = {"value": round(c["qps"], 1), "unit": "construction searches/s", "cores": threads,
                "kind": "reference",
                "sample": f"first {lim} nodes of the same node sequence x 2 timed sweeps after 1 warm sweep, "
                          f"reference search_padded with collect_pes (oracle/_ref/pag_ref build-search), "
                          f"{threads} threads on {cpu_model()}"}
+        # full-size parity of the bit-exact headline against the reference's results
+        r_ids, r_sq, r_n, r_st, r_pn, r_pes = read_reference_construction(ref_out)
+        g_ids, g_sq, g_n, g_pn = m["ids"][:lim], m["sq"][:lim], m["n"][:lim], m["pes_n"][:lim]
+        rcap = r_pes.shape[1]
+        pes_eq = [int(g_pn[i]) == int(r_pn[i]) and np.array_equal(
+            m["pes"][i, :min(int(g_pn[i]), cap, rcap)], r_pes[i, :min(int(r_pn[i]), cap, rcap)]) for i in range(lim)]
+        parity = {"nodes": lim, "checker": "pag_ref build-search --out (the reference built from its own sources)",
+                  "ids_equal": round(float(np.mean([np.array_equal(g_ids[i, :g_n[i]], r_ids[i, :r_n[i]])
+                                                    for i in range(lim)])), 5),
+                  "sq_bit_equal": round(float(np.mean([np.array_equal(g_sq[i, :g_n[i]].view(np.uint32),
+                                                                      r_sq[i, :r_n[i]].view(np.uint32))
+                                                       for i in range(lim)])), 5),
+                  "counters_equal": round(float((m["stats"][:lim, :4].astype(np.uint64) == r_st).all(axis=1).mean()), 5),
+                  "pes_rejected_equal": round(float(np.mean(pes_eq)), 5)}
     sm = m["stats"].astype(np.float64)
     line = {
         "metric": f"construction searches/s (insert_with_state search: K=efS=efC={K}, b=b_build={ix.b_build}, "
@@ -769,6 +801,7 @@ def run_construction(args, cfg, paths, rank, world, local_rank, threads, dist):
                      "pes_rejected": round(float(m["pes_n"].mean()), 3)},
         "clocks": clk_summary,
         "cpu_baseline": cpu,
+        "reference_parity": parity,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
