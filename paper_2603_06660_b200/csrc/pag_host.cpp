@@ -561,10 +561,11 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     L.warps_per_block = kWarpsPerBlock;
     L.tune = std::getenv("PAG_GPU_TUNE") ? static_cast<uint32_t>(std::atoi(std::getenv("PAG_GPU_TUNE"))) : 0u;
     L.stage_rows = 4;
-    // the visited hash holds ~half its slots before spilling to the bitmap:
-    // 512 marks cover efS <= 200 at K = 10; past that the marks outgrow any
-    // on-chip table and a small one keeps occupancy (W is on-chip)
-    L.hash_log2 = p.efS <= 200 ? 10 : 8;
+    // the visited table holds half its slots before spilling to the bitmap:
+    // 512 marks cover efS <= 200 at K = 10; past that, with b > 32, the marks
+    // outgrow any on-chip table and a small one keeps occupancy (with b <= 32
+    // the full table stays faster at every efS: cfg-2 efS 300 8.2 vs 8.6 ms)
+    L.hash_log2 = (p.efS <= 200 || L.b <= 32) ? 10 : 8;
     if (const char* e = std::getenv("PAG_GPU_HASH_LOG2")) L.hash_log2 = static_cast<uint32_t>(std::atoi(e));
     L.hash_log2 = std::max(3u, std::min(16u, L.hash_log2));  // >= 2 buckets of 4 slots
     {

@@ -1915,9 +1915,14 @@ cudaError_t dispatch(const SearchLaunch& L, int grid, cudaStream_t stream, int* 
 }
 }  // namespace
 
-// efS > 200: the marks outgrow the on-chip visited table (SURVEY.md §8(a)
-// a4: 1.6k-20k marks per query) and the HBM bitmap lookups dominate
-bool search_high_occupancy(const SearchLaunch& L) { return L.efS > 200 && !std::getenv("PAG_GPU_OCC4"); }
+// efS > 200 with a large working set (b > 128, K = 1000): the marks outgrow
+// the on-chip visited table (up to 20k marks per query),
+// W is off-chip, and latency hiding by more warps pays more than registers
+// (cfg-4: 209 vs 233 ms). With b <= 128 the 128-register flavour stays faster
+// at every efS (cfg-2 efS 300: 8.2 vs 9.0 ms; cfg-3 efS 800: 23.0 vs 24.4 ms).
+bool search_high_occupancy(const SearchLaunch& L) {
+    return L.efS > 200 && L.b > 128 && !std::getenv("PAG_GPU_OCC4");
+}
 
 size_t search_kernel_smem(const SearchLaunch& L) {
     return static_cast<size_t>(L.warp_smem_bytes) * L.warps_per_block;

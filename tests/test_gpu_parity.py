@@ -222,7 +222,8 @@ def test_single_query_api_and_empty_batch(pag, built):
 
 CONSTRUCTION = [("euc48", {}), ("cos20", {}), ("deg64", {}), ("tail10", {}),
                 ("euc48", dict(K=50, efS=90, b_override=16)), ("euc48", dict(collect_pes=False)),
-                ("deg64", dict(K=64, efS=300, b_override=48))]
+                ("deg64", dict(K=64, efS=300, b_override=48)),
+                ("deg64", dict(K=150, efS=400, b_override=160))]  # b > 128, efS > 200: 6-blocks/SM flavour
 
 
 @pytest.mark.parametrize("name,kw", CONSTRUCTION)
