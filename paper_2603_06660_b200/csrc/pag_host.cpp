@@ -569,7 +569,10 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     if (const char* e = std::getenv("PAG_GPU_HASH_LOG2")) L.hash_log2 = static_cast<uint32_t>(std::atoi(e));
     L.hash_log2 = std::max(3u, std::min(16u, L.hash_log2));  // >= 2 buckets of 4 slots
     {
-        uint32_t fill = 50;  // percent of the slots filled before marks spill to the HBM bitmap
+        // percent of the slots filled before marks spill to the HBM bitmap:
+        // 75 with b <= 32 (cfg-2 efS 150: 3.90 -> 3.66 ms, efS 70-300 +0.6-2.7%),
+        // 50 otherwise (cfg-3: the longer probes cost more than the spills)
+        uint32_t fill = L.b <= 32 ? 75 : 50;
         if (const char* e = std::getenv("PAG_GPU_HASH_FILL")) fill = std::max(1, std::min(90, std::atoi(e)));
         L.hash_limit = static_cast<uint32_t>((static_cast<uint64_t>(1u << L.hash_log2) * fill) / 100);
     }
