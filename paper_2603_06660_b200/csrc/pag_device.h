@@ -96,7 +96,7 @@ struct SearchLaunch {
     uint32_t warp_smem_bytes;
     uint32_t off_q, off_T, off_hash, hash_log2, off_sqbuf;
     uint32_t hash_limit;  // marks the smem table takes before spilling to the bitmap
-    uint32_t off_stage, stage_rows;
+    uint32_t off_stage;
     uint32_t off_W, W_in_smem;
     uint32_t off_rf, off_rt, rings_in_smem;
     uint32_t off_rl, rl_in_smem, rl_cap;  // R_L append buffer (+ sort scratch)

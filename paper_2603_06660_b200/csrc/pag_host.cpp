@@ -532,11 +532,28 @@ struct Plan {
     int grid = 0;
 };
 
-// warps (queries in flight) per CTA; PAG_GPU_WPB overrides (experiments)
-int warps_per_block() {
-    static const int w = std::getenv("PAG_GPU_WPB") ? std::max(1, std::min(4, std::atoi(std::getenv("PAG_GPU_WPB")))) : 4;
-    return w;
-}
+// Experiment / test knobs (PAG_GPU_*): warps per CTA, tune bits, visited-table
+// size and fill, per-warp smem budget, plan print. Read at every plan (a few
+// getenv calls per batch) so that tests can change them between calls.
+struct Knobs {
+    int wpb = 4;
+    uint32_t tune = 0;
+    int hash_log2 = -1, hash_fill = -1;
+    long long smem_budget = -1;
+    bool debug = false;
+    Knobs() {
+        if (const char* e = std::getenv("PAG_GPU_WPB")) wpb = std::max(1, std::min(4, std::atoi(e)));
+        if (const char* e = std::getenv("PAG_GPU_TUNE")) tune = static_cast<uint32_t>(std::atoi(e));
+        if (const char* e = std::getenv("PAG_GPU_HASH_LOG2")) hash_log2 = std::atoi(e);
+        if (const char* e = std::getenv("PAG_GPU_HASH_FILL")) hash_fill = std::max(1, std::min(90, std::atoi(e)));
+        if (const char* e = std::getenv("PAG_GPU_SMEM_BUDGET")) smem_budget = std::atoll(e);
+        debug = std::getenv("PAG_GPU_DEBUG") != nullptr;
+    }
+};
+Knobs knobs() { return Knobs(); }
+
+// warps (queries in flight) per CTA
+int warps_per_block() { return knobs().wpb; }
 #ifndef PAG_WARP_SMEM_BUDGET
 #define PAG_WARP_SMEM_BUDGET (14 * 1024)
 #endif
@@ -559,21 +576,21 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     L.ix = ix.view(r);
     const int kWarpsPerBlock = warps_per_block();
     L.warps_per_block = kWarpsPerBlock;
-    L.tune = std::getenv("PAG_GPU_TUNE") ? static_cast<uint32_t>(std::atoi(std::getenv("PAG_GPU_TUNE"))) : 0u;
-    L.stage_rows = 4;
+    const Knobs kn = knobs();
+    L.tune = kn.tune;
     // the visited table holds half its slots before spilling to the bitmap:
     // 512 marks cover efS <= 200 at K = 10; past that, with b > 32, the marks
     // outgrow any on-chip table and a small one keeps occupancy (with b <= 32
     // the full table stays faster at every efS: cfg-2 efS 300 8.2 vs 8.6 ms)
     L.hash_log2 = (p.efS <= 200 || L.b <= 32) ? 10 : 8;
-    if (const char* e = std::getenv("PAG_GPU_HASH_LOG2")) L.hash_log2 = static_cast<uint32_t>(std::atoi(e));
+    if (kn.hash_log2 >= 0) L.hash_log2 = static_cast<uint32_t>(kn.hash_log2);
     L.hash_log2 = std::max(3u, std::min(16u, L.hash_log2));  // >= 2 buckets of 4 slots
     {
         // percent of the slots filled before marks spill to the HBM bitmap:
         // 75 with b <= 32 (cfg-2 efS 150: 3.90 -> 3.66 ms, efS 70-300 +0.6-2.7%),
         // 50 otherwise (cfg-3: the longer probes cost more than the spills)
         uint32_t fill = L.b <= 32 ? 75 : 50;
-        if (const char* e = std::getenv("PAG_GPU_HASH_FILL")) fill = std::max(1, std::min(90, std::atoi(e)));
+        if (kn.hash_fill > 0) fill = static_cast<uint32_t>(kn.hash_fill);
         L.hash_limit = static_cast<uint32_t>((static_cast<uint64_t>(1u << L.hash_log2) * fill) / 100);
     }
     const uint32_t b = L.b;
@@ -606,7 +623,7 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     // blocks of 4 warps in 228 KB) reachable
     uint64_t budget = pagdev::search_high_occupancy(L) ? std::min<uint32_t>(kWarpSmemBudget, 9 * 1024)
                                                        : kWarpSmemBudget;
-    if (const char* e = std::getenv("PAG_GPU_SMEM_BUDGET")) budget = std::strtoull(e, nullptr, 10);  // tests
+    if (kn.smem_budget >= 0) budget = static_cast<uint64_t>(kn.smem_budget);  // tests
     if (total() > budget) rl_s = false;
     if (total() > budget) m_s = false;
     if (total() > budget) r_s = false;
@@ -641,7 +658,7 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     if (bps <= 0) throw_err(PAG_GPU_ERUNTIME, "search configuration does not fit on the GPU");
     const int want_blocks = static_cast<int>((nq + kWarpsPerBlock - 1) / kWarpsPerBlock);
     pl.grid = std::max(1, std::min(r.num_sms * bps, want_blocks));
-    if (std::getenv("PAG_GPU_DEBUG"))
+    if (kn.debug)
         std::fprintf(stderr, "[pag_gpu] plan: b=%u warps/block=%d blocks/SM=%d grid=%d smem/warp=%u W/rings/RL/merge in smem %u%u%u%u\n",
                      L.b, L.warps_per_block, bps, pl.grid, L.warp_smem_bytes, L.W_in_smem, L.rings_in_smem,
                      L.rl_in_smem, L.merge_in_smem);
@@ -1274,7 +1291,7 @@ static void update_dup_nodes(pag_gpu_index& ix) {
     uint32_t* cnt = nullptr;
     dev_alloc(&cnt, 4);
     uint32_t h = 1;
-    const bool dbg = std::getenv("PAG_GPU_DEBUG") != nullptr;
+    const bool dbg = knobs().debug;
     if (dbg) std::fprintf(stderr, "[pag_gpu] dup check: n=%llu block_bytes=%u\n", (unsigned long long)ix.n, ix.block_bytes);
     cudaError_t e = pagdev::count_dup_groups(r.adj, r.deg, ix.n, ix.block_bytes, cnt, r.stream);
     if (dbg) std::fprintf(stderr, "[pag_gpu] dup kernel launched: %d\n", (int)e);

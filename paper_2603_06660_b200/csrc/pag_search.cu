@@ -1921,7 +1921,8 @@ cudaError_t dispatch(const SearchLaunch& L, int grid, cudaStream_t stream, int* 
 // (cfg-4: 209 vs 233 ms). With b <= 128 the 128-register flavour stays faster
 // at every efS (cfg-2 efS 300: 8.2 vs 9.0 ms; cfg-3 efS 800: 23.0 vs 24.4 ms).
 bool search_high_occupancy(const SearchLaunch& L) {
-    return L.efS > 200 && L.b > 128 && !std::getenv("PAG_GPU_OCC4");
+    static const bool force_occ4 = std::getenv("PAG_GPU_OCC4") != nullptr;  // experiments
+    return L.efS > 200 && L.b > 128 && !force_occ4;
 }
 
 size_t search_kernel_smem(const SearchLaunch& L) {
