@@ -11,6 +11,7 @@ python bench.py --steps 20 --warmup 5 > gpurun_out/rec/bench_cfg2.json 2> gpurun
 python bench.py --config cfg3 --steps 10 --warmup 3 > gpurun_out/rec/bench_cfg3.json 2> gpurun_out/rec/bench_cfg3.err; echo cfg3=$?
 python bench.py --config cfg4 --steps 5 --warmup 3 > gpurun_out/rec/bench_cfg4.json 2> gpurun_out/rec/bench_cfg4.err; echo cfg4=$?
 python bench.py --mode construction --steps 5 --warmup 3 > gpurun_out/rec/bench_cons.json 2> gpurun_out/rec/bench_cons.err; echo cons=$?
+python bench.py --config cfg1 --steps 20 --warmup 5 > gpurun_out/rec/bench_cfg1.json 2> gpurun_out/rec/bench_cfg1.err; echo cfg1=$?
 P="python bench.py --efs 70 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/rec/launches_cfg2.csv $P > gpurun_out/rec/ncu1.log 2>&1; echo ncu1=$?
 ncu --set full --clock-control none --import-source on -k regex:pag_search -s 2 -c 1 -o gpurun_out/rec/prof_cfg2 $P > gpurun_out/rec/ncu2.log 2>&1; echo ncu2=$?
