@@ -380,7 +380,9 @@ def test_working_set_off_chip_is_exact(pag, built, monkeypatch):
     Bit-identical to the oracle, for queries and the construction search."""
     monkeypatch.setenv("PAG_GPU_SMEM_BUDGET", "2048")
     for name, K, efS, kw in (("euc48", 100, 300, {}), ("euc48", 250, 500, {}), ("deg64", 64, 128, {}),
-                             ("deg64", 10, 700, dict(b_override=48)), ("cos20", 33, 70, {})):
+                             ("deg64", 10, 700, dict(b_override=48)), ("cos20", 33, 70, {}),
+                             ("deg64", 1000, 1000, {}),     # S = 32: deferred owner re-scan
+                             ("deg64", 1100, 1300, {})):    # S = 35 > 32: plain re-scan
         fx = built(name)
         ix = pag.load_index(fx["index"])
         try:
