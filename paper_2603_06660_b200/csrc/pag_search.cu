@@ -174,6 +174,17 @@ __device__ __forceinline__ void bm_or(uint32_t* p, uint32_t bits) {
     asm volatile("red.global.or.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(bits), "l"(bm_policy()) : "memory");
 }
 
+// off-chip working-set words (the warp's HBM scratch, WOFF): L2 evict-last,
+// so a warp's W stays resident while rows and bitmaps stream through
+__device__ __forceinline__ uint32_t ld_keep(const uint32_t* p) {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    uint32_t v;
+    asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol) : "memory");
+    return v;
+}
+__device__ __forceinline__ float ld_keep(const float* p) { return __uint_as_float(ld_keep(reinterpret_cast<const uint32_t*>(p))); }
+
 // The smem visited table is bucketed: 4-slot buckets (one 16-B load), an id
 // hashes to a bucket, inserts take the bucket's first empty slot (atomicCAS
 // in slot order) or move on to the next bucket. Slots fill in order and are
@@ -744,9 +755,9 @@ struct TfbMemT {
         for (uint32_t j = lane; j < S; j += 32) {
             const uint32_t i = o * S + j;
             if (i >= wsize) break;
-            const uint32_t k = fkey(W.sq[i]);
-            const uint32_t a = W.aux[i];
-            const uint32_t id = WOFF ? W.id[i] : 0u;
+            const uint32_t k = fkey(WOFF ? ld_keep(W.sq + i) : W.sq[i]);
+            const uint32_t a = WOFF ? ld_keep(W.aux + i) : W.aux[i];
+            const uint32_t id = WOFF ? ld_keep(W.id + i) : 0u;
             if (xs == EMPTY || k > xk) {
                 xk = k;
                 xs = i;
@@ -846,9 +857,9 @@ struct TfbMemT {
             nx_slot = EMPTY;
             const uint32_t i = o * S + static_cast<uint32_t>(lane);
             if (static_cast<uint32_t>(lane) < S && i < wsize) {
-                pk = fkey(W.sq[i]);
-                pid = W.id[i];
-                pax = (i == slot) ? (nx_aux | VISITED) : W.aux[i];
+                pk = fkey(ld_keep(W.sq + i));
+                pid = ld_keep(W.id + i);
+                pax = (i == slot) ? (nx_aux | VISITED) : ld_keep(W.aux + i);
             }
             pend_o = o;
             __syncwarp();
