@@ -1,0 +1,69 @@
+"""CPU tests of the measurement code in bench.py: the algorithmic-bytes
+formula, the readers of the reference binary's result files
+(the checker of the full-size parity line), the fallback operating points and
+the workload definitions against BASELINE.json."""
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+
+import bench
+
+
+def test_algorithmic_bytes_formula():
+    # two queries: (exact, test, pass, visited, edges)
+    st = np.array([[10, 50, 8, 5, 100], [0, 0, 0, 0, 0]], np.uint64)
+    dpad, L, K = 768, 32, 10
+    q0 = 4 * dpad + 4 * 5 + 100 * (16 + 16) + 10 * 4 * dpad + 8 * K
+    q1 = 4 * dpad + 8 * K
+    assert bench.algorithmic_bytes(st, dpad, L, K) == q0 + q1
+    # odd subspace count: ceil(L/2) code bytes per edge
+    assert bench.algorithmic_bytes(st[:1], 128, 15, 1) == 4 * 128 + 20 + 100 * (16 + 8) + 10 * 512 + 8
+
+
+def test_reference_result_readers(tmp_path):
+    nq, k = 3, 4
+    ids = np.arange(nq * k, dtype=np.uint32).reshape(nq, k)
+    sq = np.linspace(0, 1, nq * k, dtype=np.float32).reshape(nq, k)
+    n_out = np.array([4, 2, 0], np.uint32)
+    st = np.arange(nq * 4, dtype=np.uint64).reshape(nq, 4)
+    p = tmp_path / "r.bin"
+    with open(p, "wb") as f:
+        f.write(np.array([nq, k], np.uint64).tobytes() + ids.tobytes() + sq.tobytes() + n_out.tobytes()
+                + st.tobytes())
+    r = bench.read_reference_results(str(p))
+    for a, b in zip(r, (ids, sq, n_out, st)):
+        assert np.array_equal(a, b)
+    cap = 5
+    pes_n = np.array([1, 7, 0], np.uint32)
+    pes = np.arange(nq * cap, dtype=np.uint32).reshape(nq, cap)
+    p2 = tmp_path / "c.bin"
+    with open(p2, "wb") as f:
+        f.write(np.array([nq, k, cap], np.uint64).tobytes() + ids.tobytes() + sq.tobytes() + n_out.tobytes()
+                + st.tobytes() + pes_n.tobytes() + pes.tobytes())
+    r2 = bench.read_reference_construction(str(p2))
+    for a, b in zip(r2, (ids, sq, n_out, st, pes_n, pes)):
+        assert np.array_equal(a, b)
+
+
+def test_workloads_match_baseline_configs():
+    base = json.load(open(os.path.join(bench.ROOT, "BASELINE.json")))
+    cfgs = bench.CONFIGS
+    # configs[1]: the headline workload (1M x 768, unit, 4096 centres, sigma 0.4, 10k queries, K = 10)
+    c2 = cfgs["cfg2"]
+    assert (c2["n"], c2["d"], c2["K"], c2["nq"], c2["centres"], c2["sigma"], c2["unit"]) == \
+        (1_000_000, 768, 10, 10_000, 4096, 0.4, True)
+    assert "1,000,000" in base["configs"][1] and "d=768" in base["configs"][1]
+    assert (cfgs["cfg3"]["n"], cfgs["cfg3"]["d"], cfgs["cfg3"]["K"]) == (1_000_000, 1024, 100)
+    assert (cfgs["cfg4"]["n"], cfgs["cfg4"]["d"], cfgs["cfg4"]["K"], cfgs["cfg4"]["nq"]) == (2_000_000, 512, 1000, 20_000)
+    assert (cfgs["cfg1"]["n"], cfgs["cfg1"]["d"], cfgs["cfg1"]["K"]) == (20_000, 128, 10)
+
+
+def test_reference_arm_fallback_operating_points(tmp_path):
+    paths = {"index": str(tmp_path / "x.pagidx")}
+    assert bench.default_efs(bench.CONFIGS["cfg2"], paths) == 70
+    with open(tmp_path / "operating_point.json", "w") as f:
+        json.dump({"efS": 80, "sweep": []}, f)
+    assert bench.default_efs(bench.CONFIGS["cfg2"], paths) == 80
