@@ -1080,22 +1080,50 @@ void refresh_index(pag_gpu_index& ix, const char* path, uint64_t* st) {
     }
     ix.mirror_adj.resize(n_new * BB);
     ix.mirror_deg.resize(n_new);
-    std::vector<uint32_t> dirty;
-    std::vector<uint8_t> blk(BB);
+    // pass 1 (sequential): record offsets and degrees; pass 2 (host threads
+    // over node ranges): build each block, diff it against the mirror and
+    // collect the changed ones (merged in node order)
+    std::vector<uint64_t> recoff(n_new);
+    std::vector<uint32_t> degs(n_new);
     uint64_t edges = 0;
     for (uint64_t u = 0; u < n_new; ++u) {
         const uint32_t deg = cur.pod<uint32_t>();
         if (deg > ix.maxdeg) throw_err(PAG_GPU_ERUNTIME, "degree over cap in file");
         edges += deg;
-        std::fill(blk.begin(), blk.end(), 0);
-        fill_block(blk.data(), cur.take(rec * deg), deg, n_new, S, cb, cwp);
-        uint8_t* mb = &ix.mirror_adj[u * BB];
-        if (u >= n_old || ix.mirror_deg[u] != deg || std::memcmp(mb, blk.data(), BB) != 0) {
-            std::memcpy(mb, blk.data(), BB);
-            ix.mirror_deg[u] = deg;
-            dirty.push_back(static_cast<uint32_t>(u));
-        }
+        degs[u] = deg;
+        recoff[u] = static_cast<uint64_t>(cur.take(rec * deg) - mp.p);
     }
+    const unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::vector<uint32_t>> dirty_t(nth);
+    std::vector<std::string> err_t(nth);
+    auto diff_range = [&](unsigned t) {
+        const uint64_t u0 = n_new * t / nth, u1 = n_new * (t + 1) / nth;
+        std::vector<uint8_t> blk(BB);
+        try {
+            for (uint64_t u = u0; u < u1; ++u) {
+                std::fill(blk.begin(), blk.end(), 0);
+                fill_block(blk.data(), mp.p + recoff[u], degs[u], n_new, S, cb, cwp);
+                uint8_t* mb = &ix.mirror_adj[u * BB];
+                if (u >= n_old || ix.mirror_deg[u] != degs[u] || std::memcmp(mb, blk.data(), BB) != 0) {
+                    std::memcpy(mb, blk.data(), BB);
+                    ix.mirror_deg[u] = degs[u];
+                    dirty_t[t].push_back(static_cast<uint32_t>(u));
+                }
+            }
+        } catch (const PagError& e) {
+            err_t[t] = e.msg;
+        }
+    };
+    {
+        std::vector<std::thread> th;
+        for (unsigned t = 1; t < nth; ++t) th.emplace_back(diff_range, t);
+        diff_range(0);
+        for (auto& x : th) x.join();
+    }
+    for (const auto& e : err_t)
+        if (!e.empty()) throw_err(PAG_GPU_ERUNTIME, e);
+    std::vector<uint32_t> dirty;
+    for (const auto& d : dirty_t) dirty.insert(dirty.end(), d.begin(), d.end());
     const uint8_t* rows = cur.take(4ull * padded * n_new);
     const uint8_t* norms = cur.take(4ull * n_new);
     const size_t row_bytes = 4ull * ix.dstride;
