@@ -148,8 +148,15 @@ struct Common {
     // flushed W entries are appended here and the cap-limited sorted list is
     // formed once at the end (the bounded insert keeps the efS smallest, an
     // order-independent result). rl_tmp is the final sort's scratch.
-    Arr rl, rl_tmp, mo;
+    // (bases only: the three-array views are formed where used, so they do
+    // not occupy registers through the search loop)
+    uint8_t* rl_base;
+    uint8_t* mo_base;
+    uint32_t rl_cap, mo_cap;
     uint32_t rl_size, cap_r;
+    __device__ Arr rl() const { return make_arr(rl_base, rl_cap); }
+    __device__ Arr rl_tmp() const { return make_arr(rl_base + 12ull * rl_cap, rl_cap); }
+    __device__ Arr mo() const { return make_arr(mo_base, mo_cap); }
     // counters (routing.hpp:24-34 + edges_scanned)
     uint32_t n_exact, n_test, n_pass, n_visited, n_edges, n_pes;
 #ifdef PAG_PHASE_TIMING
@@ -263,8 +270,9 @@ __device__ __forceinline__ void clear_bitmap(Common& c, int lane) {
 // appended and the capacity-limited sorted list is formed at the end.
 __device__ __forceinline__ void rl_append(Common& c, uint32_t id, float sq, bool valid, uint32_t offset) {
     if (valid) {
-        c.rl.id[c.rl_size + offset] = id;
-        c.rl.sq[c.rl_size + offset] = sq;
+        const Arr rl = c.rl();
+        rl.id[c.rl_size + offset] = id;
+        rl.sq[c.rl_size + offset] = sq;
     }
 }
 
@@ -619,28 +627,29 @@ struct TfbReg {
             }
         }
         __syncwarp();
+        const Arr mo = c.mo();
         if (fv) {
-            c.mo.id[fr] = f_id;
-            c.mo.sq[fr] = f_sq;
-            c.mo.aux[fr] = f_deg;
+            mo.id[fr] = f_id;
+            mo.sq[fr] = f_sq;
+            mo.aux[fr] = f_deg;
         }
         if (tv) {
-            c.mo.id[tr] = t_id;
-            c.mo.sq[tr] = t_sq;
-            c.mo.aux[tr] = t_deg;
+            mo.id[tr] = t_id;
+            mo.sq[tr] = t_sq;
+            mo.aux[tr] = t_deg;
         }
         __syncwarp();
         const uint32_t refill = min(nm, b);
         if (L < refill) {
-            w_id = c.mo.id[L];
-            w_sq = c.mo.sq[L];
-            w_deg = c.mo.aux[L];
+            w_id = mo.id[L];
+            w_sq = mo.sq[L];
+            w_deg = mo.aux[L];
             w_vis = false;
         }
         if (L < nm - refill) {  // ring_t was cleared; the rest (<= b) in ascending order
-            t_id = c.mo.id[refill + L];
-            t_sq = c.mo.sq[refill + L];
-            t_deg = c.mo.aux[refill + L];
+            t_id = mo.id[refill + L];
+            t_sq = mo.sq[refill + L];
+            t_deg = mo.aux[refill + L];
         }
         wsize = refill;
         rt_size = nm - refill;
@@ -1000,7 +1009,7 @@ struct TfbMemT {
             clear_caches();
             return false;
         }
-        const Arr srt = warp_sort(mi, c.mo, nm, lane);
+        const Arr srt = warp_sort(mi, c.mo(), nm, lane);
         const uint32_t refill = min(nm, b);
         for (uint32_t i = lane; i < nm; i += 32) {
             if (i < refill) {
@@ -1640,10 +1649,11 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
     {
         uint8_t* rl = (P.rl_in_smem ? sw : gw) + P.off_rl;
         const uint32_t cap = P.rl_cap;  // >= all W flushes of a query (r_max * b + b)
-        c.rl = make_arr(rl, cap);
-        c.rl_tmp = make_arr(rl + 12ull * cap, cap);
+        c.rl_base = rl;
+        c.rl_cap = cap;
         uint8_t* mg = (P.merge_in_smem ? sw : gw) + P.off_merge;
-        c.mo = make_arr(mg + 24ull * P.b, 2 * P.b);
+        c.mo_base = mg + 24ull * P.b;
+        c.mo_cap = 2 * P.b;
     }
     c.cap_r = P.efS;
     c.hs = reinterpret_cast<uint32_t*>(sw + P.off_hash);
@@ -1851,9 +1861,9 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
         // R_L = the min(efS, flushed) smallest, output its first K
         // (routing.cpp:244-246): the K smallest of all flushed entries
         const uint32_t k_out = min(P.K, min(c.cap_r, c.rl_size));
-        for (uint32_t i = lane; i < c.rl_size; i += 32) c.rl.aux[i] = 0u;
+        for (uint32_t i = lane; i < c.rl_size; i += 32) c.rl().aux[i] = 0u;
         __syncwarp();
-        const Arr res = warp_sort(c.rl, c.rl_tmp, c.rl_size, lane);
+        const Arr res = warp_sort(c.rl(), c.rl_tmp(), c.rl_size, lane);
         release();
         for (uint32_t i = lane; i < k_out; i += 32) {
             P.out_ids[static_cast<uint64_t>(qid) * P.K + i] = res.id[i];
