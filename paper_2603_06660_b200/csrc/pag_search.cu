@@ -135,7 +135,7 @@ struct Common {
     float* T;
     float* stage;
     float* sqbuf;
-    uint32_t* degbuf;
+    __device__ uint32_t* degbuf() const { return reinterpret_cast<uint32_t*>(sqbuf + 32); }
     // visited marks (routing.hpp:104-105): smem open addressing; once the
     // smem table is half full further marks go to this warp's n-bit HBM
     // bitmap (one load per lookup, no probe chains), cleared after the query
@@ -448,7 +448,8 @@ struct TfbReg {
     uint32_t w_id, w_deg;
     float w_sq;
     bool w_vis;
-    Arr rf;  // ring R_F: b <= 32 slots in smem (bulk pushes scatter into it)
+    uint8_t* rf_base;  // ring R_F: 32 slots {id | sq | aux} in smem (bulk pushes scatter into it)
+    __device__ Arr rf() const { return make_arr(rf_base, 32); }
     uint32_t t_id, t_deg;
     float t_sq;
     uint32_t wsize, rf_head, rf_size, rt_head, rt_size;
@@ -457,7 +458,7 @@ struct TfbReg {
 
     __device__ void init(uint32_t b_, uint8_t* sw, uint8_t* gw, const SearchLaunch& P) {
         b = b_;
-        rf = make_arr((P.rings_in_smem ? sw : gw) + P.off_rf, 32);
+        rf_base = (P.rings_in_smem ? sw : gw) + P.off_rf;
     }
     __device__ void reset() {
         wsize = rf_head = rf_size = rt_head = rt_size = 0;
@@ -531,9 +532,9 @@ struct TfbReg {
         uint32_t pos = rf_head + rf_size;
         if (pos >= b) pos -= b;
         if (lane == 0) {
-            rf.id[pos] = id;
-            rf.sq[pos] = sq;
-            rf.aux[pos] = deg;
+            rf().id[pos] = id;
+            rf().sq[pos] = sq;
+            rf().aux[pos] = deg;
         }
         if (rf_size < b) ++rf_size;
         else rf_head = (rf_head + 1 == b) ? 0 : rf_head + 1;
@@ -550,9 +551,9 @@ struct TfbReg {
             if (r + b >= np) {
                 uint32_t pos = rf_head + rf_size + r;
                 while (pos >= b) pos -= b;
-                rf.id[pos] = id;
-                rf.sq[pos] = sq;
-                rf.aux[pos] = deg;
+                rf().id[pos] = id;
+                rf().sq[pos] = sq;
+                rf().aux[pos] = deg;
             }
         }
         const uint32_t tot = rf_size + np;
@@ -600,9 +601,9 @@ struct TfbReg {
         uint32_t f_id = 0, f_deg = 0;
         float f_sq = 0.0f;
         if (L < b) {
-            f_id = rf.id[L];
-            f_sq = rf.sq[L];
-            f_deg = rf.aux[L];
+            f_id = rf().id[L];
+            f_sq = rf().sq[L];
+            f_deg = rf().aux[L];
         }
         const bool tv = L < b && ((L + b - rt_head) % b) < rt_size;
         const uint32_t nm = rf_size + rt_size;
@@ -1033,7 +1034,7 @@ struct TfbMemT {
 
 // ---------------------------------------------------------------------------
 // Exact squared distances for the rows named by lanes in `items` (lane j:
-// row id w). Results land in c.sqbuf[j], deg[w] in c.degbuf[j].
+// row id w). Results land in c.sqbuf[j], deg[w] in c.degbuf()[j].
 // EXACT: the reference order (vecstore.cpp:77-95). All 32 lanes compute the
 //   squared differences of a 128-float chunk (coalesced float4 loads, one
 //   chunk of look-ahead, packed f32x2 arithmetic) and scatter them transposed
@@ -1360,7 +1361,7 @@ __device__ __forceinline__ void distances(const SearchLaunch& P, Common& c, uint
             dist_fast<NCH>(P, c, items, w, lane);
         }
     }
-    if (mine) c.degbuf[lane] = deg;
+    if (mine) c.degbuf()[lane] = deg;
     __syncwarp();
 }
 
@@ -1542,7 +1543,7 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
         uint32_t passed = 0;
         if (!any_dup) {
             const float sqv = spec ? c.sqbuf[lane] : 0.0f;
-            const uint32_t dgv = spec ? c.degbuf[lane] : 0u;
+            const uint32_t dgv = spec ? c.degbuf()[lane] : 0u;
             uint32_t rem = surv;
             while (rem) {
                 const float adist = s.admission_dist(), asq = s.admission_sq();
@@ -1603,7 +1604,7 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
             ++c.n_pass;
             ++c.n_exact;
             const float sq_j = c.sqbuf[jl];
-            const uint32_t deg_j = c.degbuf[jl];
+            const uint32_t deg_j = c.degbuf()[jl];
             if (sq_j < s.admission_sq()) {
                 s.admit(w_j, sq_j, deg_j, lane);
             } else {
@@ -1644,7 +1645,6 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
     c.q = reinterpret_cast<float*>(sw + P.off_q);
     c.T = reinterpret_cast<float*>(sw + P.off_T);
     c.sqbuf = reinterpret_cast<float*>(sw + P.off_sqbuf);
-    c.degbuf = reinterpret_cast<uint32_t*>(sw + P.off_sqbuf + 128);
     c.stage = reinterpret_cast<float*>(sw + P.off_stage);
     {
         uint8_t* rl = (P.rl_in_smem ? sw : gw) + P.off_rl;
@@ -1810,7 +1810,7 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
                 rem &= rem - 1;
                 const uint32_t id = __shfl_sync(FULL, seed_id[g], t);
                 ++c.n_exact;
-                s.append(id, c.sqbuf[t], c.degbuf[t], lane);
+                s.append(id, c.sqbuf[t], c.degbuf()[t], lane);
             }
             __syncwarp();
         }
@@ -1832,7 +1832,7 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
                 const int t = __ffs(rem) - 1;
                 rem &= rem - 1;
                 ++c.n_exact;
-                s.append(__shfl_sync(FULL, myid, t), c.sqbuf[t], c.degbuf[t], lane);
+                s.append(__shfl_sync(FULL, myid, t), c.sqbuf[t], c.degbuf()[t], lane);
             }
             __syncwarp();
         }
