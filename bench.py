@@ -731,16 +731,23 @@ def run_construction(args, cfg, paths, rank, world, local_rank, threads, dist):
     # e2e: host node ids in, host results + PES lists out, through the C ABI
     e2e_steps = 0 if args.no_e2e else max(3, min(args.steps, 10))
     hp = pag.SearchParams(K=K, efS=K, b_override=ix.b_build)
+    # pag_gpu_construction_submit / wait, up to 4 batches in flight, 4 rotating
+    # preallocated result sets (node ids in, results + pes lists out, per step)
     outs = [pag.ConstructionResult(np.zeros((nn, K), np.uint32), np.zeros((nn, K), np.float32),
                                    np.zeros(nn, np.uint32), np.zeros((nn, 5), np.uint64),
-                                   np.zeros((nn, cap), np.uint32), np.zeros(nn, np.uint32)) for _ in range(2)]
-    for i in range(2 if e2e_steps else 0):  # warm-up: first touch of the reused result arrays
-        ix.construction_search(nodes, hp, pes_cap=cap, out=outs[i])
+                                   np.zeros((nn, cap), np.uint32), np.zeros(nn, np.uint32)) for _ in range(4)]
+    for i in range(4 if e2e_steps else 0):  # warm-up: pinned slot blocks, first touch of the arrays
+        ix.construction_submit(nodes, hp, pes_cap=cap, out=outs[i]).wait()
     if dist is not None:
         dist.barrier()
     t = time.perf_counter()
+    pending = []
     for i in range(e2e_steps):
-        ix.construction_search(nodes, hp, pes_cap=cap, out=outs[i % 2])
+        pending.append(ix.construction_submit(nodes, hp, pes_cap=cap, out=outs[i % 4]))
+        if len(pending) == 4:
+            pending.pop(0).wait()
+    while pending:
+        pending.pop(0).wait()
     e2e_s = max_over_ranks(max(time.perf_counter() - t, 1e-9), dist, dev)
     if rank != 0:
         if dist is not None:
@@ -789,7 +796,10 @@ def run_construction(args, cfg, paths, rank, world, local_rank, threads, dist):
                    "l2": "index (>3 GB) exceeds the 126 MB L2; no flush needed",
                    "parallelism": f"node shards, index replica per GPU x{world}"},
         "e2e": {"value": round(world * nn * e2e_steps / e2e_s, 1), "unit": "construction searches/s",
-                "h2d_bytes_per_step": nn * 4, "d2h_bytes_per_step": nn * (8 * K + 4 + 4 * 5 + 4 + 4 * cap)},
+                "h2d_bytes_per_step": nn * 4, "d2h_bytes_per_step": nn * (8 * K + 4 + 4 * 5 + 4 + 4 * cap),
+                "path": f"pag_gpu_construction_submit/wait, {e2e_steps} steps, up to 4 batches in flight, "
+                        "results and pes lists written to pinned host memory and unpacked into 4 rotating "
+                        "preallocated result sets"},
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind,

@@ -148,6 +148,15 @@ int pag_gpu_construction_search_device(pag_gpu_index* ix, const uint32_t* nodes_
                                        float* sq_dev, uint32_t* n_out_dev, uint32_t* stats_dev,
                                        uint32_t* pes_dev, uint32_t pes_cap, uint32_t* pes_n_dev, void* stream);
 
+/* Asynchronous pag_gpu_construction_search: same arguments (params NULL =
+ * the header's efC / b_build, collect_pes < 0 = enable_pes), returns a ticket
+ * completed by pag_gpu_search_wait (the same ring of up to 4 batches per GPU
+ * as pag_gpu_search_submit); the caller's arrays are filled at wait. */
+int pag_gpu_construction_submit(pag_gpu_index* ix, const uint32_t* nodes, uint64_t nn,
+                                const pag_search_params* params, int collect_pes, uint32_t* ids, float* sq,
+                                uint32_t* n_out, pag_search_stats* stats, uint32_t* pes, uint32_t pes_cap,
+                                uint32_t* pes_n, uint64_t* ticket);
+
 /* Replaces: GroundTruth ground_truth(const VectorSet& base,
  *                                    const VectorSet& queries, uint32_t k_star)
  *           proj/include/pag/bench.hpp:19, proj/src/bench.cpp:18-53,

@@ -32,6 +32,7 @@ EXPORTS = (
     "pag_gpu_search_submit",
     "pag_gpu_search_wait",
     "pag_gpu_construction_search",
+    "pag_gpu_construction_submit",
     "pag_gpu_construction_search_device",
     "pag_gpu_ground_truth",
     "pag_gpu_refresh",
@@ -82,6 +83,9 @@ def _load():
         "pag_gpu_construction_search": (C.c_int, [P, C.c_void_p, C.c_uint64, C.c_void_p, C.c_int,
                                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                                   C.c_void_p, C.c_uint32, C.c_void_p]),
+        "pag_gpu_construction_submit": (C.c_int, [P, C.c_void_p, C.c_uint64, C.c_void_p, C.c_int,
+                                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                  C.c_void_p, C.c_uint32, C.c_void_p, C.POINTER(C.c_uint64)]),
         "pag_gpu_construction_search_device": (C.c_int, [P, C.c_void_p, C.c_uint64, C.c_void_p, C.c_int,
                                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                                          C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),

@@ -195,6 +195,13 @@ struct Replica {
         float* sq = nullptr;
         uint32_t* n_out = nullptr;
         pag_search_stats* stats = nullptr;
+        // construction batches (pag_gpu_construction_submit)
+        bool cons = false;
+        uint32_t* pes = nullptr;
+        uint32_t* pes_n = nullptr;
+        uint32_t pes_cap = 0;
+        uint32_t* d_nodes = nullptr;
+        size_t d_nodes_bytes = 0;
     };
     static constexpr int kAsyncDepth = 4;
     AsyncSlot aslot[kAsyncDepth];
@@ -281,6 +288,7 @@ void free_replica(Replica& r) {
     for (auto& a : r.aslot) {
         if (a.h_res) cudaFreeHost(a.h_res);
         dev_free(a.d_q);
+        dev_free(a.d_nodes);
     }
     if (r.h_flags) cudaFreeHost(r.h_flags);
     dev_free(r.d_done);
@@ -1228,6 +1236,19 @@ void async_complete(pag_gpu_index& ix, Replica& r, Replica::AsyncSlot& a, uint32
     }
     std::memcpy(a.n_out, a.h_res + 2 * ob_ids, ob_n);
     const uint32_t* st = reinterpret_cast<const uint32_t*>(a.h_res + 2 * ob_ids + ob_n);
+    if (a.cons) {  // pes lists: the written prefix of each row, zeros past it
+        const size_t ob_st = 4ull * nq * pagdev::kStatWords;
+        const uint8_t* hp = a.h_res + 2 * ob_ids + ob_n + ob_st;
+        const uint32_t* hpn = reinterpret_cast<const uint32_t*>(hp + 4ull * nq * a.pes_cap);
+        std::memcpy(a.pes_n, hpn, 4ull * nq);
+        if (a.pes_cap)
+            for (uint64_t i = 0; i < nq; ++i) {
+                const uint32_t m = std::min(hpn[i], a.pes_cap);
+                uint32_t* row = a.pes + i * a.pes_cap;
+                std::memcpy(row, hp + 4ull * i * a.pes_cap, 4ull * m);
+                std::memset(row + m, 0, 4ull * (a.pes_cap - m));
+            }
+    }
     uint32_t so = 0;
     for (uint64_t i = 0; i < nq; ++i) {
         const uint32_t* w = st + i * pagdev::kStatWords;
@@ -1246,7 +1267,7 @@ void async_complete(pag_gpu_index& ix, Replica& r, Replica::AsyncSlot& a, uint32
 
 void async_submit_replica(pag_gpu_index& ix, Replica& r, const pag_search_params& p, const float* q,
                           uint64_t nq, uint32_t* ids, float* sq, uint32_t* n_out, pag_search_stats* stats,
-                          uint64_t ticket, uint32_t* status_or) {
+                          uint64_t ticket, uint32_t* status_or, const ConstructionHost* ch = nullptr) {
     cuda_check(cudaSetDevice(r.device), "cudaSetDevice");
     if (!r.h_flags) {
         cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&r.h_flags), 4 * Replica::kAsyncDepth, cudaHostAllocMapped),
@@ -1261,7 +1282,8 @@ void async_submit_replica(pag_gpu_index& ix, Replica& r, const pag_search_params
     if (nq == 0) return;
     const uint32_t K = p.K;
     const size_t ob_ids = 4ull * nq * std::max(1u, K), ob_n = 4ull * nq, ob_st = 4ull * nq * pagdev::kStatWords;
-    const size_t need = 2 * ob_ids + ob_n + ob_st;
+    const size_t ob_pes = ch ? 4ull * nq * ch->pes_cap : 0, ob_pn = ch ? 4ull * nq : 0;
+    const size_t need = 2 * ob_ids + ob_n + ob_st + ob_pes + ob_pn;
     if (a.h_bytes < need) {
         if (a.h_res) cudaFreeHost(a.h_res);
         a.h_res = nullptr;
@@ -1275,8 +1297,17 @@ void async_submit_replica(pag_gpu_index& ix, Replica& r, const pag_search_params
     cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dflags), r.h_flags, 0), "cudaHostGetDevicePointer");
     const float* q_src = nullptr;
     cudaPointerAttributes at{};
-    if (!std::getenv("PAG_GPU_NO_ZEROCOPY") && cudaPointerGetAttributes(&at, q) == cudaSuccess &&
-        at.type == cudaMemoryTypeHost && at.devicePointer) {
+    ConstructionArgs ca;
+    if (ch) {  // construction: node ids to the device (4 B each), pes lists into the pinned block
+        grow_dev(reinterpret_cast<void**>(&a.d_nodes), &a.d_nodes_bytes, 4ull * nq);
+        cuda_check(cudaMemcpyAsync(a.d_nodes, ch->nodes, 4ull * nq, cudaMemcpyHostToDevice, r.stream), "H2D nodes");
+        ca.nodes = a.d_nodes;
+        ca.collect_pes = ch->collect_pes;
+        ca.pes_cap = ch->pes_cap;
+        ca.pes = reinterpret_cast<uint32_t*>(dres + 2 * ob_ids + ob_n + ob_st);
+        ca.pes_n = reinterpret_cast<uint32_t*>(dres + 2 * ob_ids + ob_n + ob_st + ob_pes);
+    } else if (!std::getenv("PAG_GPU_NO_ZEROCOPY") && cudaPointerGetAttributes(&at, q) == cudaSuccess &&
+               at.type == cudaMemoryTypeHost && at.devicePointer) {
         q_src = static_cast<const float*>(at.devicePointer);
     } else {
         (void)cudaGetLastError();
@@ -1296,10 +1327,14 @@ void async_submit_replica(pag_gpu_index& ix, Replica& r, const pag_search_params
     a.sq = sq;
     a.n_out = n_out;
     a.stats = stats;
+    a.cons = ch != nullptr;
+    a.pes = ch ? ch->pes : nullptr;
+    a.pes_n = ch ? ch->pes_n : nullptr;
+    a.pes_cap = ch ? ch->pes_cap : 0;
     try {
         run_search(ix, r, p, q_src, static_cast<uint32_t>(nq), nullptr, reinterpret_cast<uint32_t*>(dres),
                    reinterpret_cast<float*>(dres + ob_ids), reinterpret_cast<uint32_t*>(dres + 2 * ob_ids),
-                   reinterpret_cast<uint32_t*>(dres + 2 * ob_ids + ob_n), r.stream, 0, nullptr, &aa);
+                   reinterpret_cast<uint32_t*>(dres + 2 * ob_ids + ob_n), r.stream, 0, ch ? &ca : nullptr, &aa);
     } catch (...) {
         a.ticket = 0;
         throw;
@@ -1545,6 +1580,42 @@ int pag_gpu_search_submit(pag_gpu_index* ix, const float* q, uint64_t nq, const 
                                  n_out + q0, stats ? stats + q0 : nullptr, t, &so);
         }
         check_status(so);  // (from an older batch completed to free its slot)
+    });
+}
+
+int pag_gpu_construction_submit(pag_gpu_index* ix, const uint32_t* nodes, uint64_t nn,
+                                const pag_search_params* params, int collect_pes, uint32_t* ids, float* sq,
+                                uint32_t* n_out, pag_search_stats* stats, uint32_t* pes, uint32_t pes_cap,
+                                uint32_t* pes_n, uint64_t* ticket) {
+    return guarded([&] {
+        if (!ix || !ticket) throw_err(PAG_GPU_EINVAL, "null argument");
+        std::lock_guard<std::mutex> g(ix->mu);
+        pag_search_params p{};
+        if (params) {
+            p = *params;
+        } else {  // insert_with_state (builder.cpp:220-224)
+            pag_gpu_default_params(&p);
+            p.K = p.efS = ix->efC;
+            p.b_override = ix->b_build;
+        }
+        const uint32_t pes_on = collect_pes < 0 ? ix->enable_pes : static_cast<uint32_t>(collect_pes != 0);
+        validate_params(*ix, p);
+        if (nn && (!nodes || !n_out || !pes_n || (p.K && (!ids || !sq)) || (pes_cap && !pes)))
+            throw_err(PAG_GPU_EINVAL, "null argument");
+        if (nn >= 0xFFFFFFFFull) throw_err(PAG_GPU_EINVAL, "batch too large");
+        for (uint64_t i = 0; i < nn; ++i)
+            if (nodes[i] >= ix->n) throw_err(PAG_GPU_EINVAL, "node id out of range");
+        const uint64_t t = ++ix->async_seq;
+        *ticket = t;
+        const size_t nd = ix->reps.size();
+        uint32_t so = 0;
+        for (size_t d = 0; d < nd; ++d) {
+            const uint64_t q0 = nn * d / nd, q1 = nn * (d + 1) / nd;
+            ConstructionHost ch{nodes + q0, pes_on, pes_cap, pes ? pes + q0 * pes_cap : nullptr, pes_n + q0};
+            async_submit_replica(*ix, ix->reps[d], p, nullptr, q1 - q0, ids + q0 * p.K, sq + q0 * p.K, n_out + q0,
+                                 stats ? stats + q0 : nullptr, t, &so, &ch);
+        }
+        check_status(so);
     });
 }
 

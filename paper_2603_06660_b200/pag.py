@@ -246,6 +246,38 @@ class PagIndex:
             return out
         return ConstructionResult(ids, sq, n_out, stats.copy(), pes, pes_n)
 
+    def construction_submit(self, nodes, params: Optional[SearchParams] = None, collect_pes: Optional[bool] = None,
+                            pes_cap: int = 256, out: Optional[ConstructionResult] = None) -> "PendingBatch":
+        """Asynchronous construction_search (pag_gpu_construction_submit):
+        returns at once; PendingBatch.wait() gives the ConstructionResult
+        (written into `out` when given)."""
+        nodes = np.ascontiguousarray(nodes, np.uint32).reshape(-1)
+        nn = len(nodes)
+        K = int(params.K) if params is not None else self.efC
+        if out is not None:
+            res = out
+            for a, shape, dt in ((res.ids, (nn, K), np.uint32), (res.sq, (nn, K), np.float32),
+                                 (res.n_out, (nn,), np.uint32), (res.stats, (nn, 5), np.uint64),
+                                 (res.pes, (nn, pes_cap), np.uint32), (res.pes_n, (nn,), np.uint32)):
+                if a.shape != shape or a.dtype != dt or not a.flags.c_contiguous:
+                    raise ValueError("out arrays do not match the batch")
+        else:
+            res = ConstructionResult(np.empty((nn, K), np.uint32), np.empty((nn, K), np.float32),
+                                     np.empty(nn, np.uint32), np.empty((nn, 5), np.uint64),
+                                     np.empty((nn, pes_cap), np.uint32), np.empty(nn, np.uint32))
+        pc = params.to_c() if params is not None else None
+        cp = -1 if collect_pes is None else int(bool(collect_pes))
+        t = C.c_uint64(0)
+        check(lib.pag_gpu_construction_submit(self._h, nodes.ctypes.data if nn else None, nn,
+                                              C.byref(pc) if pc is not None else None, cp,
+                                              res.ids.ctypes.data if K and nn else None,
+                                              res.sq.ctypes.data if K and nn else None,
+                                              res.n_out.ctypes.data if nn else None,
+                                              res.stats.ctypes.data if nn else None,
+                                              res.pes.ctypes.data if pes_cap and nn else None, pes_cap,
+                                              res.pes_n.ctypes.data if nn else None, C.byref(t)))
+        return PendingBatch(self, int(t.value), nodes, res)
+
     def construction_search_device(self, nodes_ptr: int, nn: int, params: Optional[SearchParams],
                                    collect_pes: Optional[bool], ids_ptr: int, sq_ptr: int, n_out_ptr: int,
                                    stats_ptr: int, pes_ptr: int, pes_cap: int, pes_n_ptr: int,

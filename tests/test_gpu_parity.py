@@ -471,3 +471,18 @@ def test_construction_search_reuses_out_arrays(pag, built):
         assert not got.pes[i, min(int(got.pes_n[i]), cap):].any()
     with pytest.raises(ValueError):
         ix.construction_search(nodes[:-1], out=out)
+
+
+def test_construction_submit_wait_matches_blocking(pag, built):
+    """pag_gpu_construction_submit: several batches in flight (the 4-slot ring
+    wraps), each equal to the blocking construction_search, pes tails zero."""
+    fx = built("deg64")
+    ix = gpu_index(pag, fx["index"])
+    batches = [np.arange(s, ix.n, 17, dtype=np.uint32)[:90] for s in range(6)]
+    want = [ix.construction_search(b) for b in batches]
+    pend = [ix.construction_submit(b) for b in batches]
+    for p, w, b in zip(pend, want, batches):
+        got = p.wait()
+        for x, y in ((got.ids, w.ids), (got.sq, w.sq), (got.n_out, w.n_out), (got.stats, w.stats),
+                     (got.pes_n, w.pes_n), (got.pes, w.pes)):
+            assert np.array_equal(x, y)
