@@ -133,20 +133,38 @@ int cmd_build(const Args& a) {
     return 0;
 }
 
+// search over a query file (the roles of pag_cli.cpp:244-266 and
+// run_benchmark's timing, bench.cpp:151-190). --efS takes a comma list; per
+// efS: one untimed warm sweep, `reps` timed sweeps with `threads` threads
+// (one TfbState per thread, atomic query counter), optionally a 1-thread
+// warm + timed sweep over the first `single-limit` queries, and with --out
+// the results (suffix ".efS<e>" when several efS are given; --single-efS
+// restricts the 1-thread timing to one of them). One JSON line per efS.
 int cmd_search(const Args& a) {
     PagIndex index = load_index(a.get("index"));
     uint32_t d;
     size_t nq;
     std::vector<float> qs = read_fvecs_raw(a.get("queries"), &d, &nq);
     if (a.has("limit")) nq = std::min<size_t>(nq, std::stoull(a.get("limit")));
+    std::vector<uint32_t> efs_list;
+    {
+        std::string e = a.get("efS", "100");
+        size_t p = 0;
+        while (p <= e.size()) {
+            size_t c = e.find(',', p);
+            if (c == std::string::npos) c = e.size();
+            if (c > p) efs_list.push_back(static_cast<uint32_t>(std::stoul(e.substr(p, c - p))));
+            p = c + 1;
+        }
+    }
     SearchParams sp;
     sp.K = std::stoul(a.get("K", "10"));
-    sp.efS = std::stoul(a.get("efS", "100"));
     if (a.has("b")) sp.b_override = std::stoul(a.get("b"));
     sp.use_prt = !a.has("no-prt");
     sp.use_tfb = !a.has("no-tfb");
     unsigned threads = static_cast<unsigned>(std::stoul(a.get("threads", "1")));
     int reps = std::stoi(a.get("reps", "1"));
+    const size_t single = a.has("single-limit") ? std::min<size_t>(nq, std::stoull(a.get("single-limit"))) : 0;
     const uint32_t K = sp.K;
 
     std::vector<uint32_t> ids(nq * K, 0xFFFFFFFFu);
@@ -167,47 +185,63 @@ int cmd_search(const Args& a) {
         st[qi * 4 + 2] = r.stats.pass_count;
         st[qi * 4 + 3] = r.stats.visited_count;
     };
-    auto sweep = [&]() {
-        if (threads <= 1) {
+    auto sweep = [&](unsigned nth, size_t count) {
+        if (nth <= 1) {
             TfbState state;
-            for (size_t qi = 0; qi < nq; ++qi) run_one(qi, state);
+            for (size_t qi = 0; qi < count; ++qi) run_one(qi, state);
         } else {
             std::atomic<size_t> next{0};
             std::vector<std::thread> pool;
-            for (unsigned t = 0; t < threads; ++t)
+            for (unsigned t = 0; t < nth; ++t)
                 pool.emplace_back([&] {
                     TfbState state;
                     size_t qi;
-                    while ((qi = next.fetch_add(1)) < nq) run_one(qi, state);
+                    while ((qi = next.fetch_add(1)) < count) run_one(qi, state);
                 });
             for (auto& th : pool) th.join();
         }
     };
-    // one untimed warm sweep, then timed sweeps (bench.cpp:161-188)
-    if (!a.has("no-warm")) sweep();
-    double best = 1e30, total = 0;
-    for (int r = 0; r < reps; ++r) {
+    auto timed = [&](unsigned nth, size_t count) {
         auto t0 = clk::now();
-        sweep();
-        double s = std::chrono::duration<double>(clk::now() - t0).count();
-        total += s;
-        best = std::min(best, s);
+        sweep(nth, count);
+        return std::chrono::duration<double>(clk::now() - t0).count();
+    };
+    for (uint32_t efS : efs_list) {
+        sp.efS = efS;
+        // one untimed warm sweep, then timed sweeps (bench.cpp:161-188)
+        if (!a.has("no-warm")) sweep(threads, nq);
+        double best = 1e30, total = 0;
+        for (int r = 0; r < reps; ++r) {
+            const double s = timed(threads, nq);
+            total += s;
+            best = std::min(best, s);
+        }
+        if (a.has("out")) {
+            std::string path = a.get("out");
+            if (efs_list.size() > 1) path += ".efS" + std::to_string(efS);
+            std::FILE* f = std::fopen(path.c_str(), "wb");
+            if (!f) throw std::runtime_error("cannot open output");
+            uint64_t hdr[2] = {nq, K};
+            write_all(f, hdr, sizeof hdr);
+            write_all(f, ids.data(), ids.size() * 4);
+            write_all(f, sq.data(), sq.size() * 4);
+            write_all(f, nout.data(), nout.size() * 4);
+            write_all(f, st.data(), st.size() * 8);
+            std::fclose(f);
+        }
+        double s1 = 0;
+        const bool single_here = single && (!a.has("single-efS") || std::stoul(a.get("single-efS")) == efS);
+        if (single_here) {
+            sweep(1, single);  // warm
+            s1 = timed(1, single);
+        }
+        std::printf(
+            "{\"efS\": %u, \"queries\": %zu, \"threads\": %u, \"reps\": %d, \"seconds_mean\": %.6f, "
+            "\"seconds_best\": %.6f, \"qps\": %.3f, \"single_queries\": %zu, \"single_qps\": %.3f}\n",
+            efS, nq, threads, reps, total / std::max(1, reps), best, reps ? nq / (total / reps) : 0.0,
+            single_here ? single : 0, single_here ? single / s1 : 0.0);
+        std::fflush(stdout);
     }
-    if (a.has("out")) {
-        std::FILE* f = std::fopen(a.get("out").c_str(), "wb");
-        if (!f) throw std::runtime_error("cannot open output");
-        uint64_t hdr[2] = {nq, K};
-        write_all(f, hdr, sizeof hdr);
-        write_all(f, ids.data(), ids.size() * 4);
-        write_all(f, sq.data(), sq.size() * 4);
-        write_all(f, nout.data(), nout.size() * 4);
-        write_all(f, st.data(), st.size() * 8);
-        std::fclose(f);
-    }
-    std::printf(
-        "{\"queries\": %zu, \"threads\": %u, \"reps\": %d, \"seconds_mean\": %.6f, "
-        "\"seconds_best\": %.6f, \"qps\": %.3f}\n",
-        nq, threads, reps, total / reps, best, nq / (total / reps));
     return 0;
 }
 

@@ -67,3 +67,44 @@ def test_reference_arm_fallback_operating_points(tmp_path):
     with open(tmp_path / "operating_point.json", "w") as f:
         json.dump({"efS": 80, "sweep": []}, f)
     assert bench.default_efs(bench.CONFIGS["cfg2"], paths) == 80
+
+
+def _res(ids, sq, n=None, st=None):
+    ids = np.asarray(ids, np.uint32)
+    sq = np.asarray(sq, np.float32)
+    n = np.full(ids.shape[0], ids.shape[1], np.uint32) if n is None else np.asarray(n, np.uint32)
+    st = np.zeros((ids.shape[0], 4), np.uint64) if st is None else st
+    return ids, sq, n, st
+
+
+def test_compare_with_reference_bitexact_and_ties():
+    r = _res([[1, 2, 3], [4, 5, 6]], [[0.1, 0.2, 0.3], [0.1, 0.2, 0.5]])
+    c = bench.compare_with_reference(r, r, 3)
+    assert c["ids_equal"] == c["sq_bit_equal"] == c["counters_equal"] == c["id_sets_equal"] == 1.0
+    assert c["unexplained_diffs"] == 0 and c["max_rel_sq_diff"] == 0.0
+    # query 0: id 3 swapped for id 9 at a distance tie with the K-th (explained);
+    # query 1: id 5 (well inside the radius) missing (unexplained)
+    g = _res([[1, 2, 9], [4, 6, 7]], [[0.1, 0.2, 0.3 * (1 + 2e-6)], [0.1, 0.5, 0.5]])
+    c = bench.compare_with_reference(g, r, 3)
+    assert c["id_sets_equal"] == 0.0 and c["unexplained_diffs"] == 1
+    # recall against a ground truth, same tie policy as recall_at_k
+    gt_ids = np.array([[1, 2, 3], [4, 5, 6]], np.uint32)
+    gt_sq = np.array([[0.1, 0.2, 0.3], [0.1, 0.2, 0.5]], np.float32)
+    c = bench.compare_with_reference(g, r, 3, gt_ids, gt_sq)
+    assert c["reference_recall"] == 1.0 and abs(c["recall_delta"] - (4 / 6 - 1.0)) < 1e-5
+
+
+def test_reference_arm_imports_no_native_library():
+    """bench.py's reference arm must not map libpag_gpu.so (the driver checks
+    which repo .so files the reference process loaded): the package exposes
+    its API lazily and the measurement helpers are library-free."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r); import bench; import paper_2603_06660_b200 as p; "
+            "from paper_2603_06660_b200 import fvecs, shard, recall; p.mean_recall; p.recall_at_k; "
+            "bench.compare_with_reference; "
+            "maps = open('/proc/self/maps').read(); assert 'libpag_gpu' not in maps, 'library loaded'; "
+            "p.load_index; assert 'libpag_gpu' in open('/proc/self/maps').read(); print('ok')"
+            % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
+    assert out.returncode == 0 and out.stdout.strip() == "ok", out.stderr
