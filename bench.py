@@ -291,6 +291,12 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--mode", default="search", choices=["search", "construction"],
                     help="construction: the search step of insert_with_state (SURVEY.md §8(f) next-2)")
+    ap.add_argument("--shard", default="torchrun", choices=["torchrun", "abi"],
+                    help="torchrun: one process per GPU (the driver's launch); abi: ONE process, one handle "
+                         "over all GPUs (pag_gpu_open_devices), the C ABI shards every batch across replicas")
+    ap.add_argument("--devices", default="",
+                    help="--shard abi: replica device list, e.g. 0,1,2,3 (default range(--gpus)); an ordinal "
+                         "may repeat (several replicas on one GPU)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -328,6 +334,10 @@ def main():
     if args.config == "cfg5":
         if rank == 0:
             run_online(args, cfg, paths, threads)
+        return
+    if args.shard == "abi":
+        if rank == 0:
+            run_shard_abi(args, cfg, paths, threads)
         return
     run_pag(args, cfg, paths, rank, world, local_rank, threads, dist)
 
@@ -405,6 +415,82 @@ def run_online(args, cfg, paths, threads):
                                  "batches": cfg["batches"], "K": K, "efS": efs, "sweep": sweep,
                                  "distance_mode": args.dist},
                       "phases": phases}), flush=True)
+
+
+def run_shard_abi(args, cfg, paths, threads):
+    """Strong scaling through the product's own sharding: ONE process, one
+    handle with a replica per device (pag_gpu_open_devices), each step one
+    batch of (replicas x 10k) host queries that the C ABI splits into
+    contiguous shards, one per replica, searched in parallel (no collective;
+    results land in disjoint slices). Timed end to end through
+    pag_gpu_search_submit/wait with 4 batches in flight (pinned queries read
+    in place, results written to pinned host memory): value == e2e. Roofline
+    per distinct GPU from the kernels' own counters."""
+    import torch
+
+    import paper_2603_06660_b200 as pag
+
+    devs = [int(x) for x in args.devices.split(",")] if args.devices else list(range(args.gpus))
+    K = cfg["K"]
+    t0 = time.time()
+    ix = pag.load_index(paths["index"], devices=devs)
+    log(f"{len(devs)} replicas on devices {devs} in {time.time() - t0:.1f}s")
+    queries = read_fvecs(paths["queries"])
+    nq1 = queries.shape[0]
+    efs = args.efs or default_efs(cfg, paths)
+    params = pag.SearchParams(K=K, efS=efs, exact_dist=args.dist == "exact")
+    nrep = len(devs)
+    qall = np.ascontiguousarray(np.tile(queries, (nrep, 1)))
+    nq = qall.shape[0]
+    q_pin = torch.empty(qall.shape, dtype=torch.float32, pin_memory=True)
+    q_pin.numpy()[:] = qall
+    qh = q_pin.numpy()
+    outs = [pag.BatchResult(np.zeros((nq, K), np.uint32), np.zeros((nq, K), np.float32), np.zeros(nq, np.uint32),
+                            np.zeros((nq, 5), np.uint64)) for _ in range(4)]
+    for i in range(max(4, args.warmup)):
+        ix.search_submit(qh, params, out=outs[i % 4]).wait()
+    steps = max(4, args.steps)
+    gpus = sorted(set(devs))
+    with Clocks(gpus[0]) as clk:
+        t = time.perf_counter()
+        pending = []
+        for i in range(steps):
+            pending.append(ix.search_submit(qh, params, out=outs[i % 4]))
+            if len(pending) == 4:
+                pending.pop(0).wait()
+        while pending:
+            pending.pop(0).wait()
+        secs = time.perf_counter() - t
+    value = nq * steps / secs
+    r = outs[(steps - 1) % 4]
+    gt = np.load(paths["gt"]) if os.path.exists(paths["gt"]) else None
+    recall = None
+    if gt is not None:
+        recall = pag.mean_recall(r.ids[:nq1], r.n_out[:nq1], gt["ids"], gt["sq"], K)
+    same = all(np.array_equal(r.ids[k * nq1:(k + 1) * nq1], r.ids[:nq1]) for k in range(nrep))
+    bytes_total = algorithmic_bytes(r.stats, ix.padded_dim, ix.L, K)
+    per_gpu = bytes_total / (secs / steps) / 1e9 / len(gpus)
+    peak, peak_kind = load_peaks()
+    print(json.dumps({
+        "metric": f"QPS at recall@{K}={args.target_recall} (batched search, {cfg['n']}x{cfg['d']})",
+        "value": round(value, 1), "unit": "queries/s", "n_gpus": len(gpus), "replicas": nrep, "steps": steps,
+        "warmup": max(4, args.warmup), "ms_per_step": round(1e3 * secs / steps, 4), "higher_is_better": True,
+        "scaling": "strong-per-replica-batch", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded Gaussian mixture per BASELINE.json; index from the reference CPU build)",
+        "config": {"workload": args.config, "n": cfg["n"], "d": cfg["d"], "queries_per_step": nq, "K": K,
+                   "efS": efs, "recall": None if recall is None else round(recall, 4), "distance_mode": args.dist,
+                   "devices": devs, "replica_results_identical": bool(same),
+                   "parallelism": f"one handle, {nrep} replicas, contiguous query shards (C ABI)"},
+        "e2e": {"value": round(value, 1), "unit": "queries/s", "h2d_bytes_per_step": int(qall.nbytes),
+                "d2h_bytes_per_step": nq * (8 * K + 4 + 32),
+                "path": "pag_gpu_search_submit/wait over all replicas, 4 batches in flight"},
+        "gpu_launches": steps * nrep,
+        "roofline": {"bound": "hbm", "achieved_per_gpu": round(per_gpu, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(per_gpu / peak, 4), "peak_kind": peak_kind,
+                     "note": "wall clock over submit..wait (host unpacking included)"},
+        "clocks": clk.summary(),
+    }), flush=True)
+    ix.close()
 
 
 def choose_efs(ix, queries, gt_ids, gt_sq, cfg, args, pag):

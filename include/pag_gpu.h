@@ -72,6 +72,14 @@ void pag_gpu_default_params(pag_search_params* p);
  * Batches are split across those GPUs (query sharding, no collective). */
 int pag_gpu_open(const char* index_path, uint32_t device_mask, pag_gpu_index** out);
 
+/* pag_gpu_open with an explicit replica list: one full replica of the index
+ * per entry of devices[0..n_devices) (CUDA device ordinals). An ordinal may
+ * repeat: several replicas then share one GPU, each with its own copy,
+ * stream, scratch and host worker (the multi-replica path exercised on a
+ * single GPU). The file streams once over the host link into the first
+ * replica; the others are filled device to device. n_devices = 0 = {0}. */
+int pag_gpu_open_devices(const char* index_path, const int* devices, uint32_t n_devices, pag_gpu_index** out);
+
 /* Releases every device replica (the PagIndex destructor). */
 int pag_gpu_close(pag_gpu_index* ix);
 
@@ -101,8 +109,9 @@ int pag_gpu_search(pag_gpu_index* ix, const float* q, uint64_t nq,
  * raw counters {exact,test,pass,visited,edges,status,marks,0}), launched on
  * `stream` (a cudaStream_t; NULL = the legacy default stream) without host
  * synchronisation. For resident-input throughput measurement and for
- * callers that keep queries on the GPU. Queries flagged with a visited-set
- * overflow (status bit 1) are NOT retried on this path. */
+ * callers that keep queries on the GPU. Consecutive launches on one stream
+ * overlap (programmatic dependent launch); a launch on a different stream
+ * than the handle's previous one first waits for that stream's work. */
 int pag_gpu_search_device(pag_gpu_index* ix, const float* q_dev, uint64_t nq,
                           const pag_search_params* params, uint32_t* ids_dev, float* sq_dev,
                           uint32_t* n_out_dev, uint32_t* stats_dev, void* stream);
@@ -114,8 +123,11 @@ int pag_gpu_search_device(pag_gpu_index* ix, const float* q_dev, uint64_t nq,
  * pageable ones are copied at submit. Up to 4 batches are in flight per GPU
  * (a 5th submit first completes the oldest); consecutive batches overlap on
  * the GPU like back-to-back pag_gpu_search_device calls. Errors of a batch
- * (e.g. "zero query under cosine metric") are reported by the call that
- * completes it. Calls on one handle serialise. */
+ * (e.g. "zero query under cosine metric") are reported by that batch's own
+ * wait, also when a later submit completed it to free its ring slot. A
+ * submit that fails launches nothing that outlives it. Calls on one handle
+ * serialise; a handle with several replicas splits each batch into one
+ * contiguous shard per replica. */
 int pag_gpu_search_submit(pag_gpu_index* ix, const float* q, uint64_t nq, const pag_search_params* params,
                           uint32_t* ids, float* sq, uint32_t* n_out, pag_search_stats* stats, uint64_t* ticket);
 int pag_gpu_search_wait(pag_gpu_index* ix, uint64_t ticket);
@@ -142,7 +154,7 @@ int pag_gpu_construction_search(pag_gpu_index* ix, const uint32_t* nodes, uint64
 /* pag_gpu_construction_search with every buffer on device 0 of the handle
  * (node ids must be < n; not checked here), launched on `stream` without
  * host synchronisation; stats_dev: nn x 8 u32 raw counters as
- * pag_gpu_search_device. No visited-overflow retry on this path. */
+ * pag_gpu_search_device (the same stream rule). */
 int pag_gpu_construction_search_device(pag_gpu_index* ix, const uint32_t* nodes_dev, uint64_t nn,
                                        const pag_search_params* params, int collect_pes, uint32_t* ids_dev,
                                        float* sq_dev, uint32_t* n_out_dev, uint32_t* stats_dev,

@@ -25,6 +25,7 @@ PAG_GPU_ECUDA = 5
 EXPORTS = (
     "pag_gpu_default_params",
     "pag_gpu_open",
+    "pag_gpu_open_devices",
     "pag_gpu_close",
     "pag_gpu_info",
     "pag_gpu_search",
@@ -69,6 +70,7 @@ def _load():
     sig = {
         "pag_gpu_default_params": (None, [C.POINTER(SearchParamsC)]),
         "pag_gpu_open": (C.c_int, [C.c_char_p, C.c_uint32, C.POINTER(P)]),
+        "pag_gpu_open_devices": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.c_uint32, C.POINTER(P)]),
         "pag_gpu_close": (C.c_int, [P]),
         "pag_gpu_info": (C.c_int, [P, u64p, C.c_size_t]),
         "pag_gpu_search": (C.c_int, [P, C.c_void_p, C.c_uint64, C.POINTER(SearchParamsC),

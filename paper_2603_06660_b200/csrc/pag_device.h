@@ -11,7 +11,6 @@ namespace pagdev {
 // Per-query status bits written next to the counters.
 enum : uint32_t {
     kStatusZeroCosineQuery = 1u << 0,  // routing.cpp:257 "zero query under cosine metric"
-    kStatusVisitedOverflow = 1u << 1,  // global visited table too small: host re-runs the query
 };
 
 // Per-query counters (routing.hpp:24-34 plus edges_scanned and status).
@@ -63,8 +62,6 @@ struct SearchLaunch {
     float* out_sq;        // nq x K
     uint32_t* out_n;      // nq
     uint32_t* out_stats;  // nq x kStatWords
-    // optional subset of query indices to run (retry path); null = all
-    const uint32_t* qlist;
     // construction search (builder.cpp:218-227): query i is the stored row of
     // node qnodes[i] (queries unused); with collect_pes the expanded nodes
     // whose PES max is negative (routing.cpp:190-199,235) go to
@@ -74,12 +71,16 @@ struct SearchLaunch {
     uint32_t* out_pes;
     uint32_t* out_pes_n;
     // scheduling + scratch
-    // query claim counter of this launch, and the previous launch's, which
-    // this one zeroes once that launch has completed (programmatic dependent
-    // launch: consecutive launches alternate between two counters and two
-    // scratch sets, so a launch can start while its predecessor drains)
+    // query claim counter of this launch's parity. Counters are never reset:
+    // every warp of a launch claims until it draws an index >= nq, so a
+    // launch advances its counter by exactly nq + (warps in the grid), and
+    // the host passes the value at launch as qbase (query = claim - qbase,
+    // mod 2^32). Consecutive launches alternate between two counters and two
+    // scratch sets (programmatic dependent launch: launch N+1 may start while
+    // N drains; N+2, same parity as N, starts only after N has completed).
     uint32_t* qcounter;
-    uint32_t* qcounter_other;
+    uint32_t qbase;
+    uint32_t pdl;  // launch with programmatic stream serialisation (0 after a stream switch)
     // asynchronous host API (pag_gpu_search_submit): when host_flag is set,
     // the last warp to exit writes flag_value to this pinned host word after
     // a system-scope fence (all outputs, written to pinned host memory, are
@@ -102,11 +103,6 @@ struct SearchLaunch {
     uint32_t off_rl, rl_in_smem, rl_cap;  // R_L append buffer (+ sort scratch)
     uint32_t off_merge, merge_in_smem;
     uint32_t warps_per_block;
-    // experiment bits (PAG_GPU_TUNE, A/B runs in tools/tune_probe.py); no
-    // production path reads them. Measured and removed: adjacency look-ahead
-    // into smem by cp.async.bulk, TMEM-resident W, row-pair and 8-row
-    // reference-order distances
-    uint32_t tune;
 };
 
 size_t search_kernel_smem(const SearchLaunch& L);

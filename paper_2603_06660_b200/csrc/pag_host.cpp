@@ -18,6 +18,9 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
+#include <exception>
+#include <functional>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -27,6 +30,7 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/pag_gpu.h"
@@ -172,8 +176,14 @@ struct Replica {
     size_t slots = 0;
     uint8_t* gscratch = nullptr;
     size_t gscratch_bytes = 0;
-    uint32_t* qcounter = nullptr;  // two claim counters (launch parity)
+    uint32_t* qcounter = nullptr;  // two claim counters (launch parity), never reset
+    uint32_t qbase[2] = {0, 0};    // their values at the next launch of each parity
     uint64_t seq = 0;              // search launches so far (parity of counters and scratch)
+    // the stream of the last search launch: a launch on another stream first
+    // waits for it (event), so launches of one replica never overlap across
+    // streams (the two scratch sets / counters assume one launch order)
+    cudaStream_t last_stream = nullptr;
+    cudaEvent_t order_ev = nullptr;
     // batch I/O
     float* d_q = nullptr;
     size_t d_q_bytes = 0;
@@ -200,13 +210,70 @@ struct Replica {
         uint32_t* pes = nullptr;
         uint32_t* pes_n = nullptr;
         uint32_t pes_cap = 0;
-        uint32_t* d_nodes = nullptr;
-        size_t d_nodes_bytes = 0;
     };
     static constexpr int kAsyncDepth = 4;
     AsyncSlot aslot[kAsyncDepth];
     uint32_t* h_flags = nullptr;  // pinned, mapped: one completion word per slot
     uint32_t* d_done = nullptr;   // device: exited-warp counters per slot
+    // persistent host worker of this replica (handles with more than one
+    // replica): blocking searches, construction searches and ground truth of
+    // all replicas run in parallel without spawning threads per call
+    struct Worker;
+    std::shared_ptr<Worker> worker;
+};
+
+// One host thread per replica, fed one job at a time by run_replicas().
+struct Replica::Worker {
+    std::mutex m;
+    std::condition_variable cv;
+    std::function<void()> job;
+    bool stop = false, busy = false;
+    std::exception_ptr err;
+    std::thread th;
+    Worker() {
+        th = std::thread([this] {
+            std::unique_lock<std::mutex> lk(m);
+            for (;;) {
+                cv.wait(lk, [this] { return stop || busy; });
+                if (busy) {
+                    std::function<void()> f = std::move(job);
+                    lk.unlock();
+                    std::exception_ptr e;
+                    try {
+                        f();
+                    } catch (...) {
+                        e = std::current_exception();
+                    }
+                    lk.lock();
+                    err = e;
+                    busy = false;
+                    cv.notify_all();
+                } else if (stop) {
+                    return;
+                }
+            }
+        });
+    }
+    void post(std::function<void()> f) {
+        std::lock_guard<std::mutex> lk(m);
+        job = std::move(f);
+        err = nullptr;
+        busy = true;
+        cv.notify_all();
+    }
+    std::exception_ptr join_job() {
+        std::unique_lock<std::mutex> lk(m);
+        cv.wait(lk, [this] { return !busy; });
+        return err;
+    }
+    ~Worker() {
+        {
+            std::lock_guard<std::mutex> lk(m);
+            stop = true;
+            cv.notify_all();
+        }
+        if (th.joinable()) th.join();
+    }
 };
 
 template <typename T>
@@ -247,6 +314,9 @@ struct pag_gpu_index {
     std::vector<uint32_t> mirror_deg;
     std::vector<float> refs;
     std::vector<Replica> reps;
+    // status bits of asynchronous batches that a later submit completed to
+    // free their ring slot, reported by their own wait (per ticket)
+    std::unordered_map<uint64_t, uint32_t> early_status;
     std::mutex mu;
 
     pagdev::IndexView view(const Replica& r) const {
@@ -276,7 +346,11 @@ struct pag_gpu_index {
 namespace {
 
 void free_replica(Replica& r) {
+    r.worker.reset();  // joins the replica's host thread
     cudaSetDevice(r.device);
+    if (r.stream) cudaStreamSynchronize(r.stream);  // in-flight asynchronous batches
+    // (launches on caller streams: cudaFree below waits for the device)
+    if (r.order_ev) cudaEventDestroy(r.order_ev);
     for (void* p : {static_cast<void*>(r.rows), static_cast<void*>(r.deg), static_cast<void*>(r.adj),
                     static_cast<void*>(r.refsT), static_cast<void*>(r.entries),
                     static_cast<void*>(r.gbm),
@@ -284,11 +358,9 @@ void free_replica(Replica& r) {
                     static_cast<void*>(r.d_q), static_cast<void*>(r.d_out), static_cast<void*>(r.bnorm)})
         dev_free(p);
     if (r.h_pin) cudaFreeHost(r.h_pin);
-    if (r.stream) cudaStreamSynchronize(r.stream);  // in-flight asynchronous batches
     for (auto& a : r.aslot) {
         if (a.h_res) cudaFreeHost(a.h_res);
         dev_free(a.d_q);
-        dev_free(a.d_nodes);
     }
     if (r.h_flags) cudaFreeHost(r.h_flags);
     dev_free(r.d_done);
@@ -321,7 +393,9 @@ void fill_block(uint8_t* blk, const uint8_t* e, uint32_t deg, uint64_t n, uint32
 // PAGIDX01 v1 ingest (builder.cpp:434-492) straight into the device layout
 // ---------------------------------------------------------------------------
 // dry = true: parse and validate the whole file on the host only (no GPU).
-std::unique_ptr<pag_gpu_index> open_index(const char* path, uint32_t device_mask, bool dry = false) {
+// devs: one replica per entry (a device may repeat: several replicas on one
+// GPU, each with its own copy, stream and scratch)
+std::unique_ptr<pag_gpu_index> open_index(const char* path, const std::vector<int>& devs, bool dry = false) {
     Mapped mp;
     mp.fd = ::open(path, O_RDONLY);
     if (mp.fd < 0) throw_err(PAG_GPU_ERUNTIME, std::string("cannot open index: ") + path);
@@ -369,21 +443,17 @@ std::unique_ptr<pag_gpu_index> open_index(const char* path, uint32_t device_mask
     ix->slot_stride = std::max(32u, (ix->maxdeg + 31u) & ~31u);
     ix->block_bytes = ix->slot_stride * (16u + 4u * ix->cwp);
 
-    std::vector<int> devs;
     if (!dry) {
-        if (device_mask == 0) device_mask = 1;
+        if (devs.empty()) throw_err(PAG_GPU_EINVAL, "no device given");
         int ndev = 0;
         cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
-        for (int d = 0; d < 32; ++d)
-            if (device_mask & (1u << d)) {
-                if (d >= ndev) throw_err(PAG_GPU_EINVAL, "device_mask names a missing GPU");
-                devs.push_back(d);
-            }
+        for (int d : devs)
+            if (d < 0 || d >= ndev) throw_err(PAG_GPU_EINVAL, "device list names a missing GPU");
     }
 
     const uint64_t n = ix->n;
     const size_t row_bytes = 4ull * ix->dstride;
-    for (int d : devs) {
+    for (int d : (dry ? std::vector<int>{} : devs)) {
         Replica r;
         r.device = d;
         cuda_check(cudaSetDevice(d), "cudaSetDevice");
@@ -396,6 +466,7 @@ std::unique_ptr<pag_gpu_index> open_index(const char* path, uint32_t device_mask
         dev_alloc(&r.entries, 4ull * std::max<size_t>(1, n_entries));
         dev_alloc(&r.qcounter, 16);
         cuda_check(cudaMemset(r.qcounter, 0, 16), "memset");
+        cuda_check(cudaEventCreateWithFlags(&r.order_ev, cudaEventDisableTiming), "cudaEventCreate");
         r.bytes = n * row_bytes + 4ull * n + static_cast<size_t>(n) * ix->block_bytes +
                   4ull * ix->refs.size();
         r.cap_nodes = n;
@@ -457,9 +528,13 @@ std::unique_ptr<pag_gpu_index> open_index(const char* path, uint32_t device_mask
     const uint32_t S = ix->slot_stride, cb = ix->cb, cwp = ix->cwp;
     const size_t rec = 4 + cb + 12;
     int buf = 0;
+    // the file streams through pinned staging into the first replica; the
+    // others are then filled device to device (NVLink peer copies across
+    // GPUs, or on-device copies), so the host link carries the index once
+    Replica* r0 = ix->reps.empty() ? nullptr : &ix->reps[0];
     for (uint64_t u0 = 0; u0 < n; u0 += CH) {
         const uint64_t cnt = std::min<uint64_t>(CH, n - u0);
-        for (auto& r : ix->reps) cudaStreamSynchronize(r.stream);  // buffer reuse
+        if (r0) cudaStreamSynchronize(r0->stream);  // buffer reuse
         uint8_t* blk0 = stage[buf];
         uint32_t* dg = dstage[buf];
         std::memset(blk0, 0, cnt * ix->block_bytes);
@@ -470,17 +545,17 @@ std::unique_ptr<pag_gpu_index> open_index(const char* path, uint32_t device_mask
             ix->total_edges += deg;
             fill_block(blk0 + i * ix->block_bytes, cur.take(rec * deg), deg, n, S, cb, cwp);
         }
-        for (auto& r : ix->reps) {
-            cudaSetDevice(r.device);
-            cuda_check(cudaMemcpyAsync(r.adj + u0 * ix->block_bytes, blk0, cnt * ix->block_bytes,
-                                       cudaMemcpyHostToDevice, r.stream),
+        if (r0) {
+            cudaSetDevice(r0->device);
+            cuda_check(cudaMemcpyAsync(r0->adj + u0 * ix->block_bytes, blk0, cnt * ix->block_bytes,
+                                       cudaMemcpyHostToDevice, r0->stream),
                        "H2D adjacency");
-            cuda_check(cudaMemcpyAsync(r.deg + u0, dg, cnt * 4, cudaMemcpyHostToDevice, r.stream),
+            cuda_check(cudaMemcpyAsync(r0->deg + u0, dg, cnt * 4, cudaMemcpyHostToDevice, r0->stream),
                        "H2D degrees");
         }
         buf ^= 1;
     }
-    for (auto& r : ix->reps) cuda_check(cudaStreamSynchronize(r.stream), "adjacency upload");
+    if (r0) cuda_check(cudaStreamSynchronize(r0->stream), "adjacency upload");
 
     // rows (n x padded fp32), restrided to dstride with zero padding
     {
@@ -490,7 +565,7 @@ std::unique_ptr<pag_gpu_index> open_index(const char* path, uint32_t device_mask
         buf = 0;
         for (uint64_t i0 = 0; i0 < n; i0 += RCH) {
             const uint64_t cnt = std::min<uint64_t>(RCH, n - i0);
-            for (auto& r : ix->reps) cudaStreamSynchronize(r.stream);
+            if (r0) cudaStreamSynchronize(r0->stream);
             uint8_t* st = stage[buf];
             if (dry) {
                 // host-only inspection: rows are validated for presence only
@@ -501,15 +576,26 @@ std::unique_ptr<pag_gpu_index> open_index(const char* path, uint32_t device_mask
                 for (uint64_t i = 0; i < cnt; ++i)
                     std::memcpy(st + i * row_bytes, rows + (i0 + i) * 4ull * ix->padded, 4ull * ix->padded);
             }
-            for (auto& r : ix->reps) {
-                cudaSetDevice(r.device);
-                cuda_check(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(r.rows) + i0 * row_bytes, st,
-                                           cnt * row_bytes, cudaMemcpyHostToDevice, r.stream),
+            if (r0) {
+                cudaSetDevice(r0->device);
+                cuda_check(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(r0->rows) + i0 * row_bytes, st,
+                                           cnt * row_bytes, cudaMemcpyHostToDevice, r0->stream),
                            "H2D rows");
             }
             buf ^= 1;
         }
-        for (auto& r : ix->reps) cuda_check(cudaStreamSynchronize(r.stream), "rows upload");
+        if (r0) cuda_check(cudaStreamSynchronize(r0->stream), "rows upload");
+        for (size_t i = 1; i < ix->reps.size(); ++i) {  // replica i <- replica 0
+            Replica& r = ix->reps[i];
+            cudaSetDevice(r.device);
+            cuda_check(cudaMemcpyPeerAsync(r.rows, r.device, r0->rows, r0->device, n * row_bytes, r.stream),
+                       "peer copy rows");
+            cuda_check(cudaMemcpyPeerAsync(r.adj, r.device, r0->adj, r0->device, n * ix->block_bytes, r.stream),
+                       "peer copy adjacency");
+            cuda_check(cudaMemcpyPeerAsync(r.deg, r.device, r0->deg, r0->device, 4ull * n, r.stream),
+                       "peer copy degrees");
+        }
+        for (auto& r : ix->reps) cuda_check(cudaStreamSynchronize(r.stream), "replica copies");
         // squared norms for the tensor-core ground truth (cached norms are the
         // stored rows' vec_norm, builder.cpp:489-491)
         if (!ix->reps.empty()) {
@@ -540,18 +626,16 @@ struct Plan {
     int grid = 0;
 };
 
-// Experiment / test knobs (PAG_GPU_*): warps per CTA, tune bits, visited-table
-// size and fill, per-warp smem budget, plan print. Read at every plan (a few
-// getenv calls per batch) so that tests can change them between calls.
+// Test / diagnostic knobs (PAG_GPU_*): warps per CTA, visited-table size and
+// fill, per-warp smem budget, plan print. Read at every plan (a few getenv
+// calls per batch) so that tests can change them between calls.
 struct Knobs {
     int wpb = 4;
-    uint32_t tune = 0;
     int hash_log2 = -1, hash_fill = -1;
     long long smem_budget = -1;
     bool debug = false;
     Knobs() {
         if (const char* e = std::getenv("PAG_GPU_WPB")) wpb = std::max(1, std::min(4, std::atoi(e)));
-        if (const char* e = std::getenv("PAG_GPU_TUNE")) tune = static_cast<uint32_t>(std::atoi(e));
         if (const char* e = std::getenv("PAG_GPU_HASH_LOG2")) hash_log2 = std::atoi(e);
         if (const char* e = std::getenv("PAG_GPU_HASH_FILL")) hash_fill = std::max(1, std::min(90, std::atoi(e)));
         if (const char* e = std::getenv("PAG_GPU_SMEM_BUDGET")) smem_budget = std::atoll(e);
@@ -569,8 +653,7 @@ constexpr uint32_t kWarpSmemBudget = PAG_WARP_SMEM_BUDGET;
 
 uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 
-Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_params& p, uint32_t nq,
-               uint32_t gt_log2_min) {
+Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_params& p, uint32_t nq) {
     Plan pl;
     auto& L = pl.L;
     const uint32_t bdef = p.b_override ? p.b_override : std::max(10u, p.K);
@@ -585,7 +668,6 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     const int kWarpsPerBlock = warps_per_block();
     L.warps_per_block = kWarpsPerBlock;
     const Knobs kn = knobs();
-    L.tune = kn.tune;
     // the visited table holds half its slots before spilling to the bitmap:
     // 512 marks cover efS <= 200 at K = 10; past that, with b > 32, the marks
     // outgrow any on-chip table and a small one keeps occupancy (with b <= 32
@@ -660,7 +742,6 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     L.gscratch_stride = pl.gscratch_stride;
     // per-slot HBM visited bitmap (n bits, 16-B multiple)
     L.gbm_words = static_cast<uint32_t>(((ix.n + 127) / 128) * 4);
-    (void)gt_log2_min;
     int bps = 0;
     cuda_check(pagdev::search_occupancy(L, &bps), "occupancy");
     if (bps <= 0) throw_err(PAG_GPU_ERUNTIME, "search configuration does not fit on the GPU");
@@ -693,7 +774,7 @@ void ensure_scratch(Replica& r, Plan& pl) {
     L.gbm = r.gbm + par * r.slots * r.gbm_words;
     L.gscratch = r.gscratch + par * r.slots * pl.gscratch_stride;
     L.qcounter = r.qcounter + par;
-    L.qcounter_other = r.qcounter + (par ^ 1u);
+    L.qbase = r.qbase[par];
 }
 
 void validate_params(const pag_gpu_index& ix, const pag_search_params& p) {
@@ -717,14 +798,21 @@ struct ConstructionArgs {
 };
 
 // Runs nq queries already on the replica's device. Device buffers:
-// q (nq x dim), ids/sq (nq x K), n_out (nq), stats (nq x 8). qlist optional.
+// q (nq x dim), ids/sq (nq x K), n_out (nq), stats (nq x 8).
 void run_search(pag_gpu_index& ix, Replica& r, const pag_search_params& p, const float* q_dev,
-                uint32_t nq, const uint32_t* qlist, uint32_t* ids, float* sq, uint32_t* n_out,
-                uint32_t* stats, cudaStream_t stream, uint32_t gt_log2_min,
+                uint32_t nq, uint32_t* ids, float* sq, uint32_t* n_out, uint32_t* stats, cudaStream_t stream,
                 const ConstructionArgs* ca = nullptr, const AsyncArgs* aa = nullptr) {
     if (nq == 0) return;
-    Plan pl = make_plan(ix, r, p, nq, gt_log2_min);
+    Plan pl = make_plan(ix, r, p, nq);
     ensure_scratch(r, pl);
+    // one launch order per replica: a launch on another stream than the last
+    // one waits for everything before it there and does not overlap it
+    bool pdl = true;
+    if (r.seq && stream != r.last_stream) {
+        cuda_check(cudaEventRecord(r.order_ev, r.last_stream), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(stream, r.order_ev, 0), "cudaStreamWaitEvent");
+        pdl = false;
+    }
     auto& L = pl.L;
     if (aa) {
         L.done_ctr = aa->done_ctr;
@@ -733,7 +821,7 @@ void run_search(pag_gpu_index& ix, Replica& r, const pag_search_params& p, const
         L.n_warps = static_cast<uint32_t>(pl.grid) * L.warps_per_block;
     }
     L.queries = q_dev;
-    L.qlist = qlist;
+    L.pdl = pdl;
     if (ca) {
         L.qnodes = ca->nodes;
         L.collect_pes = ca->collect_pes;
@@ -746,6 +834,9 @@ void run_search(pag_gpu_index& ix, Replica& r, const pag_search_params& p, const
     L.out_n = n_out;
     L.out_stats = stats;
     cuda_check(pagdev::launch_search(L, pl.grid, stream), "search kernel launch");
+    // the launch advances its counter by nq + one failed claim per warp
+    r.qbase[r.seq & 1u] += nq + static_cast<uint32_t>(pl.grid) * static_cast<uint32_t>(L.warps_per_block);
+    r.last_stream = stream;
     ++r.seq;
 }
 
@@ -786,23 +877,21 @@ void search_on_replica(pag_gpu_index& ix, Replica& r, const pag_search_params& p
     const uint32_t K = p.K;
     const size_t qb = ch ? 4ull * nq : 4ull * nq * ix.dim;
     const size_t ob_ids = 4ull * nq * std::max(1u, K), ob_n = 4ull * nq,
-                 ob_st = 4ull * nq * pagdev::kStatWords, ob_list = 4ull * nq;
+                 ob_st = 4ull * nq * pagdev::kStatWords;
     const size_t ob_pes = ch ? 4ull * nq * ch->pes_cap : 0, ob_pn = ch ? 4ull * nq : 0;
     grow_dev(reinterpret_cast<void**>(&r.d_q), &r.d_q_bytes, qb);
-    grow_dev(reinterpret_cast<void**>(&r.d_out), &r.d_out_bytes,
-             2 * ob_ids + ob_n + ob_st + ob_list + ob_pes + ob_pn);
+    grow_dev(reinterpret_cast<void**>(&r.d_out), &r.d_out_bytes, 2 * ob_ids + ob_n + ob_st + ob_pes + ob_pn);
     uint32_t* d_ids = reinterpret_cast<uint32_t*>(r.d_out);
     float* d_sq = reinterpret_cast<float*>(r.d_out + ob_ids);
     uint32_t* d_n = reinterpret_cast<uint32_t*>(r.d_out + 2 * ob_ids);
     uint32_t* d_st = reinterpret_cast<uint32_t*>(r.d_out + 2 * ob_ids + ob_n);
-    uint32_t* d_list = reinterpret_cast<uint32_t*>(r.d_out + 2 * ob_ids + ob_n + ob_st);
     ConstructionArgs ca;
     if (ch) {
         ca.nodes = reinterpret_cast<const uint32_t*>(r.d_q);
         ca.collect_pes = ch->collect_pes;
         ca.pes_cap = ch->pes_cap;
-        ca.pes = reinterpret_cast<uint32_t*>(r.d_out + 2 * ob_ids + ob_n + ob_st + ob_list);
-        ca.pes_n = reinterpret_cast<uint32_t*>(r.d_out + 2 * ob_ids + ob_n + ob_st + ob_list + ob_pes);
+        ca.pes = reinterpret_cast<uint32_t*>(r.d_out + 2 * ob_ids + ob_n + ob_st);
+        ca.pes_n = reinterpret_cast<uint32_t*>(r.d_out + 2 * ob_ids + ob_n + ob_st + ob_pes);
     }
     const ConstructionArgs* cap = ch ? &ca : nullptr;
     // entries past each pes list are zero (the kernel writes min(n, cap))
@@ -824,7 +913,7 @@ void search_on_replica(pag_gpu_index& ix, Replica& r, const pag_search_params& p
                                    cudaMemcpyHostToDevice, r.stream),
                    "H2D queries");
     tr.mark("prep");
-    run_search(ix, r, p, q_src, static_cast<uint32_t>(nq), nullptr, d_ids, d_sq, d_n, d_st, r.stream, 0, cap);
+    run_search(ix, r, p, q_src, static_cast<uint32_t>(nq), d_ids, d_sq, d_n, d_st, r.stream, cap);
     tr.mark("launch");
     // one D2H of the contiguous result block (ids | sq | n_out | counters)
     // into pinned staging
@@ -840,21 +929,6 @@ void search_on_replica(pag_gpu_index& ix, Replica& r, const pag_search_params& p
     cuda_check(cudaStreamSynchronize(r.stream), "search");
     tr.mark("kernel+d2h");
     const uint32_t* st = reinterpret_cast<const uint32_t*>(r.h_pin + 2 * ob_ids + ob_n);
-    // visited-set overflow: re-run those queries with a 4x larger HBM table
-    uint32_t grow = 2;
-    for (int attempt = 0; attempt < 6; ++attempt) {
-        std::vector<uint32_t> redo;
-        for (uint64_t i = 0; i < nq; ++i)
-            if (st[i * pagdev::kStatWords + pagdev::kStatStatus] & pagdev::kStatusVisitedOverflow)
-                redo.push_back(static_cast<uint32_t>(i));
-        if (redo.empty()) break;
-        cuda_check(cudaMemcpyAsync(d_list, redo.data(), 4 * redo.size(), cudaMemcpyHostToDevice, r.stream),
-                   "H2D retry list");
-        run_search(ix, r, p, q_src, static_cast<uint32_t>(redo.size()), d_list, d_ids, d_sq, d_n, d_st,
-                   r.stream, grow, cap);
-        cuda_check(cudaMemcpyAsync(r.h_pin, r.d_out, ob_res, cudaMemcpyDeviceToHost, r.stream), "D2H results");
-        cuda_check(cudaStreamSynchronize(r.stream), "search retry");
-    }
     if (K) {
         std::memcpy(ids, r.h_pin, 4ull * nq * K);
         std::memcpy(sq, r.h_pin + ob_ids, 4ull * nq * K);
@@ -940,10 +1014,12 @@ CUtensorMap tensor_map_rows(const float* base, uint64_t rows, uint32_t padded, u
 
 // bench.cpp:18-53. k <= 32: tensor-core candidates + exact re-rank +
 // certificate (uncertified queries re-run exactly); otherwise exact SIMT.
-void ground_truth_on_replica(pag_gpu_index& ix, Replica& r, const float* q, uint64_t nq, uint32_t k,
-                             uint32_t* ids, float* sq) {
+// Returns the number of queries whose tensor-core candidates were not
+// certified and were re-run exactly.
+uint64_t ground_truth_on_replica(pag_gpu_index& ix, Replica& r, const float* q, uint64_t nq, uint32_t k,
+                                 uint32_t* ids, float* sq) {
     cuda_check(cudaSetDevice(r.device), "cudaSetDevice");
-    if (nq == 0 || k == 0) return;
+    if (nq == 0 || k == 0) return 0;
     const uint32_t kk = static_cast<uint32_t>(std::min<uint64_t>(k, ix.n));
     const uint32_t nqu = static_cast<uint32_t>(nq);
     std::vector<float> qp(nq * ix.dstride, 0.0f);
@@ -990,7 +1066,7 @@ void ground_truth_on_replica(pag_gpu_index& ix, Replica& r, const float* q, uint
         cuda_check(cudaStreamSynchronize(r.stream), "tensor-core ground truth");
         for (uint32_t i = 0; i < nqu; ++i)
             if (flags[i]) redo.push_back(i);
-        ix.gt_uncertified += redo.size();
+
     } else {
         exact_gt(ix, r, d_q.as<float>(), nqu, kk, d_ids.as<uint32_t>(), d_sq.as<float>());
     }
@@ -1020,6 +1096,7 @@ void ground_truth_on_replica(pag_gpu_index& ix, Replica& r, const float* q, uint
         std::memcpy(ids + i * k, &hi[i * kk], 4ull * kk);
         std::memcpy(sq + i * k, &hs[i * kk], 4ull * kk);
     }
+    return redo.size();
 }
 
 // Online-insert refresh: the reference appended
@@ -1204,21 +1281,28 @@ int guarded(F&& f) {
 
 // ---------------------------------------------------------------------------
 // Asynchronous batches: submit returns after the launch; the kernel reads
-// pinned queries in place, writes results into the slot's pinned block and
-// raises the slot's completion word; wait spins on that word and unpacks.
-// Consecutive submits keep the programmatic-dependent-launch overlap (no
-// event or copy between the kernels).
+// pinned queries (or construction node ids) in place, writes results into
+// the slot's pinned block and raises the slot's completion word; wait spins
+// on that word and unpacks. Consecutive submits keep the programmatic-
+// dependent-launch overlap (no event or copy between the kernels).
 // ---------------------------------------------------------------------------
-void async_complete(pag_gpu_index& ix, Replica& r, Replica::AsyncSlot& a, uint32_t* status_or) {
-    (void)ix;
+namespace {
+
+// completion word of a ticket: never the reset value 0
+uint32_t flag_of(uint64_t ticket) { return static_cast<uint32_t>(ticket) | 0x80000000u; }
+
+void async_complete(Replica& r, Replica::AsyncSlot& a, uint32_t* status_or) {
     const int si = static_cast<int>(&a - r.aslot);
     volatile uint32_t* flag = r.h_flags + si;
-    const uint32_t want = static_cast<uint32_t>(a.ticket);
+    const uint32_t want = flag_of(a.ticket);
     uint64_t spins = 0;
     while (*flag != want) {
         if ((++spins & 1023u) == 0) {
             const cudaError_t e = cudaStreamQuery(r.stream);
-            if (e != cudaSuccess && e != cudaErrorNotReady) cuda_check(e, "asynchronous search");
+            if (e != cudaSuccess && e != cudaErrorNotReady) {
+                a.ticket = 0;
+                cuda_check(e, "asynchronous search");
+            }
             if (e == cudaSuccess && *flag != want) {
                 a.ticket = 0;
                 throw_err(PAG_GPU_ECUDA, "asynchronous search: completion flag missing");
@@ -1265,9 +1349,20 @@ void async_complete(pag_gpu_index& ix, Replica& r, Replica::AsyncSlot& a, uint32
     *status_or |= so;
 }
 
+// frees the ring slot of `ticket` on replica r: an older batch still holding
+// it is completed now and its status is kept for its own wait
+void free_slot(pag_gpu_index& ix, Replica& r, uint64_t ticket) {
+    Replica::AsyncSlot& a = r.aslot[ticket % Replica::kAsyncDepth];
+    if (!a.ticket) return;
+    const uint64_t old = a.ticket;
+    uint32_t so = 0;
+    async_complete(r, a, &so);
+    ix.early_status[old] |= so;
+}
+
 void async_submit_replica(pag_gpu_index& ix, Replica& r, const pag_search_params& p, const float* q,
                           uint64_t nq, uint32_t* ids, float* sq, uint32_t* n_out, pag_search_stats* stats,
-                          uint64_t ticket, uint32_t* status_or, const ConstructionHost* ch = nullptr) {
+                          uint64_t ticket, const ConstructionHost* ch = nullptr) {
     cuda_check(cudaSetDevice(r.device), "cudaSetDevice");
     if (!r.h_flags) {
         cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&r.h_flags), 4 * Replica::kAsyncDepth, cudaHostAllocMapped),
@@ -1278,12 +1373,13 @@ void async_submit_replica(pag_gpu_index& ix, Replica& r, const pag_search_params
     }
     const int si = static_cast<int>(ticket % Replica::kAsyncDepth);
     Replica::AsyncSlot& a = r.aslot[si];
-    if (a.ticket) async_complete(ix, r, a, status_or);  // ring full: finish the oldest first
+    free_slot(ix, r, ticket);  // ring full: finish the oldest first
     if (nq == 0) return;
     const uint32_t K = p.K;
     const size_t ob_ids = 4ull * nq * std::max(1u, K), ob_n = 4ull * nq, ob_st = 4ull * nq * pagdev::kStatWords;
     const size_t ob_pes = ch ? 4ull * nq * ch->pes_cap : 0, ob_pn = ch ? 4ull * nq : 0;
-    const size_t need = 2 * ob_ids + ob_n + ob_st + ob_pes + ob_pn;
+    const size_t ob_nodes = ch ? 4ull * nq : 0;  // construction node ids, read by the kernel in place
+    const size_t need = 2 * ob_ids + ob_n + ob_st + ob_pes + ob_pn + ob_nodes;
     if (a.h_bytes < need) {
         if (a.h_res) cudaFreeHost(a.h_res);
         a.h_res = nullptr;
@@ -1298,10 +1394,10 @@ void async_submit_replica(pag_gpu_index& ix, Replica& r, const pag_search_params
     const float* q_src = nullptr;
     cudaPointerAttributes at{};
     ConstructionArgs ca;
-    if (ch) {  // construction: node ids to the device (4 B each), pes lists into the pinned block
-        grow_dev(reinterpret_cast<void**>(&a.d_nodes), &a.d_nodes_bytes, 4ull * nq);
-        cuda_check(cudaMemcpyAsync(a.d_nodes, ch->nodes, 4ull * nq, cudaMemcpyHostToDevice, r.stream), "H2D nodes");
-        ca.nodes = a.d_nodes;
+    if (ch) {  // construction: node ids and pes lists in the pinned block (no copy between launches)
+        const size_t off = 2 * ob_ids + ob_n + ob_st + ob_pes + ob_pn;
+        std::memcpy(a.h_res + off, ch->nodes, ob_nodes);
+        ca.nodes = reinterpret_cast<const uint32_t*>(dres + off);
         ca.collect_pes = ch->collect_pes;
         ca.pes_cap = ch->pes_cap;
         ca.pes = reinterpret_cast<uint32_t*>(dres + 2 * ob_ids + ob_n + ob_st);
@@ -1318,9 +1414,8 @@ void async_submit_replica(pag_gpu_index& ix, Replica& r, const pag_search_params
     AsyncArgs aa;
     aa.done_ctr = r.d_done + si;
     aa.host_flag = dflags + si;
-    aa.flag_value = static_cast<uint32_t>(ticket);
+    aa.flag_value = flag_of(ticket);
     r.h_flags[si] = 0;
-    a.ticket = ticket;
     a.nq = nq;
     a.K = K;
     a.ids = ids;
@@ -1331,40 +1426,105 @@ void async_submit_replica(pag_gpu_index& ix, Replica& r, const pag_search_params
     a.pes = ch ? ch->pes : nullptr;
     a.pes_n = ch ? ch->pes_n : nullptr;
     a.pes_cap = ch ? ch->pes_cap : 0;
+    run_search(ix, r, p, q_src, static_cast<uint32_t>(nq), reinterpret_cast<uint32_t*>(dres),
+               reinterpret_cast<float*>(dres + ob_ids), reinterpret_cast<uint32_t*>(dres + 2 * ob_ids),
+               reinterpret_cast<uint32_t*>(dres + 2 * ob_ids + ob_n), r.stream, ch ? &ca : nullptr, &aa);
+    a.ticket = ticket;  // only a launched batch holds the slot
+}
+
+// A submit over all replicas: every replica's shard is launched, or none
+// holds caller pointers when the call fails (the shards already launched
+// are completed before the error is returned; their status is dropped with
+// the failed batch).
+template <typename LaunchShard>
+void submit_all(pag_gpu_index& ix, uint64_t t, LaunchShard&& launch) {
+    const size_t nd = ix.reps.size();
+    size_t d = 0;
     try {
-        run_search(ix, r, p, q_src, static_cast<uint32_t>(nq), nullptr, reinterpret_cast<uint32_t*>(dres),
-                   reinterpret_cast<float*>(dres + ob_ids), reinterpret_cast<uint32_t*>(dres + 2 * ob_ids),
-                   reinterpret_cast<uint32_t*>(dres + 2 * ob_ids + ob_n), r.stream, 0, ch ? &ca : nullptr, &aa);
+        for (; d < nd; ++d) launch(d);
     } catch (...) {
-        a.ticket = 0;
+        for (size_t e = 0; e < nd; ++e) {
+            Replica& r = ix.reps[e];
+            Replica::AsyncSlot& a = r.aslot[t % Replica::kAsyncDepth];
+            if (a.ticket == t) {
+                uint32_t so = 0;
+                try {
+                    cudaSetDevice(r.device);
+                    async_complete(r, a, &so);
+                } catch (...) {
+                }
+                a.ticket = 0;
+            }
+        }
         throw;
     }
 }
 
 void check_status(uint32_t so) {
     if (so & pagdev::kStatusZeroCosineQuery) throw_err(PAG_GPU_EINVAL, "zero query under cosine metric");
-    if (so & pagdev::kStatusVisitedOverflow) throw_err(PAG_GPU_ERUNTIME, "visited set overflow after retries");
 }
 
 // ix.dup_nodes from the first replica's adjacency (after load / refresh)
-static void update_dup_nodes(pag_gpu_index& ix) {
+void update_dup_nodes(pag_gpu_index& ix) {
     if (ix.reps.empty()) return;
     Replica& r = ix.reps[0];
     cuda_check(cudaSetDevice(r.device), "cudaSetDevice");
     uint32_t* cnt = nullptr;
     dev_alloc(&cnt, 4);
     uint32_t h = 1;
-    const bool dbg = knobs().debug;
-    if (dbg) std::fprintf(stderr, "[pag_gpu] dup check: n=%llu block_bytes=%u\n", (unsigned long long)ix.n, ix.block_bytes);
     cudaError_t e = pagdev::count_dup_groups(r.adj, r.deg, ix.n, ix.block_bytes, cnt, r.stream);
-    if (dbg) std::fprintf(stderr, "[pag_gpu] dup kernel launched: %d\n", (int)e);
     if (e == cudaSuccess) e = cudaStreamSynchronize(r.stream);
-    if (dbg) std::fprintf(stderr, "[pag_gpu] dup kernel done: %d\n", (int)e);
     if (e == cudaSuccess) e = cudaMemcpy(&h, cnt, 4, cudaMemcpyDeviceToHost);
     dev_free(cnt);
     cuda_check(e, "duplicate-target check");
     ix.dup_nodes = h;
 }
+
+// Runs fn(d) for every replica d: inline for one replica, else on the
+// replicas' persistent host workers in parallel (started on first use); the
+// first error (in replica order) is rethrown after all have finished.
+void run_replicas(pag_gpu_index& ix, const std::function<void(size_t)>& fn) {
+    const size_t nd = ix.reps.size();
+    if (nd == 1) {
+        fn(0);
+        return;
+    }
+    for (size_t d = 0; d < nd; ++d) {
+        Replica& r = ix.reps[d];
+        if (!r.worker) r.worker = std::make_shared<Replica::Worker>();
+        r.worker->post([&fn, d] { fn(d); });
+    }
+    std::exception_ptr first;
+    for (size_t d = 0; d < nd; ++d) {
+        std::exception_ptr e = ix.reps[d].worker->join_job();
+        if (e && !first) first = e;
+    }
+    if (first) std::rethrow_exception(first);
+}
+
+// query shard [q0, q1) of replica d (contiguous, the same bounds as the
+// torchrun sharding in shard.py)
+inline uint64_t shard_lo(uint64_t n, size_t d, size_t nd) { return n * d / nd; }
+
+pag_search_params construction_params(const pag_gpu_index& ix, const pag_search_params* params) {
+    pag_search_params p{};
+    if (params) {
+        p = *params;
+    } else {  // insert_with_state (builder.cpp:220-224): K = efS = efC, b = b_build
+        pag_gpu_default_params(&p);
+        p.K = p.efS = ix.efC;
+        p.b_override = ix.b_build;
+    }
+    return p;
+}
+
+std::unique_ptr<pag_gpu_index> open_checked(const char* index_path, const std::vector<int>& devs) {
+    auto ix = open_index(index_path, devs);
+    update_dup_nodes(*ix);
+    return ix;
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -1382,16 +1542,28 @@ int pag_gpu_open(const char* index_path, uint32_t device_mask, pag_gpu_index** o
     return guarded([&] {
         if (!out || !index_path) throw_err(PAG_GPU_EINVAL, "null argument");
         *out = nullptr;
-        auto ix = open_index(index_path, device_mask);
-        update_dup_nodes(*ix);
-        *out = ix.release();
+        if (device_mask == 0) device_mask = 1;
+        std::vector<int> devs;
+        for (int d = 0; d < 32; ++d)
+            if (device_mask & (1u << d)) devs.push_back(d);
+        *out = open_checked(index_path, devs).release();
+    });
+}
+
+int pag_gpu_open_devices(const char* index_path, const int* devices, uint32_t n_devices, pag_gpu_index** out) {
+    return guarded([&] {
+        if (!out || !index_path || (n_devices && !devices)) throw_err(PAG_GPU_EINVAL, "null argument");
+        *out = nullptr;
+        std::vector<int> devs(devices, devices + n_devices);
+        if (devs.empty()) devs.push_back(0);
+        *out = open_checked(index_path, devs).release();
     });
 }
 
 int pag_gpu_inspect(const char* index_path, uint64_t* info, size_t n_info) {
     return guarded([&] {
         if (!index_path || !info) throw_err(PAG_GPU_EINVAL, "null argument");
-        auto ix = open_index(index_path, 0, true);
+        auto ix = open_index(index_path, {}, true);
         const uint64_t v[12] = {ix->n, ix->dim, ix->padded, ix->L, ix->m, ix->M, ix->metric,
                                 ix->entries.size(), ix->seed, ix->total_edges, 0, 0};
         for (size_t i = 0; i < n_info && i < 12; ++i) info[i] = v[i];
@@ -1446,34 +1618,17 @@ int pag_gpu_search(pag_gpu_index* ix, const float* q, uint64_t nq, const pag_sea
         validate_params(*ix, p);
         if (nq == 0) return;
         if (!q || !n_out || (p.K && (!ids || !sq))) throw_err(PAG_GPU_EINVAL, "null argument");
+        if (nq >= 0xFFFFFFFFull) throw_err(PAG_GPU_EINVAL, "batch too large");
         const size_t nd = ix->reps.size();
         std::vector<uint32_t> status(nd, 0);
-        std::vector<PagError> errs;
-        std::mutex emu;
-        auto shard = [&](size_t d) {
-            const uint64_t q0 = nq * d / nd, q1 = nq * (d + 1) / nd;
-            try {
-                search_on_replica(*ix, ix->reps[d], p, q + q0 * ix->dim, q1 - q0, ids + q0 * p.K,
-                                  sq + q0 * p.K, n_out + q0, stats ? stats + q0 : nullptr, &status[d]);
-            } catch (const PagError& e) {
-                std::lock_guard<std::mutex> lk(emu);
-                errs.push_back(e);
-            }
-        };
-        if (nd == 1) {
-            shard(0);
-        } else {
-            std::vector<std::thread> th;
-            for (size_t d = 0; d < nd; ++d) th.emplace_back(shard, d);
-            for (auto& t : th) t.join();
-        }
-        if (!errs.empty()) throw errs.front();
+        run_replicas(*ix, [&](size_t d) {
+            const uint64_t q0 = shard_lo(nq, d, nd), q1 = shard_lo(nq, d + 1, nd);
+            search_on_replica(*ix, ix->reps[d], p, q + q0 * ix->dim, q1 - q0, ids + q0 * p.K, sq + q0 * p.K,
+                              n_out + q0, stats ? stats + q0 : nullptr, &status[d]);
+        });
         uint32_t so = 0;
         for (auto s : status) so |= s;
-        if (so & pagdev::kStatusZeroCosineQuery)
-            throw_err(PAG_GPU_EINVAL, "zero query under cosine metric");
-        if (so & pagdev::kStatusVisitedOverflow)
-            throw_err(PAG_GPU_ERUNTIME, "visited set overflow after retries");
+        check_status(so);
     });
 }
 
@@ -1486,48 +1641,23 @@ int pag_gpu_construction_search(pag_gpu_index* ix, const uint32_t* nodes, uint64
         std::lock_guard<std::mutex> g(ix->mu);
         // insert_with_state (builder.cpp:220-224): K = efS = efC, b = b_build,
         // collect_pes = enable_pes, unless the caller overrides
-        pag_search_params p{};
-        if (params) {
-            p = *params;
-        } else {
-            pag_gpu_default_params(&p);
-            p.K = p.efS = ix->efC;
-            p.b_override = ix->b_build;
-        }
+        const pag_search_params p = construction_params(*ix, params);
         const uint32_t pes_on = collect_pes < 0 ? ix->enable_pes : static_cast<uint32_t>(collect_pes != 0);
         validate_params(*ix, p);
         if (nn == 0) return;
         if (!nodes || !n_out || !pes_n || (p.K && (!ids || !sq)) || (pes_cap && !pes))
             throw_err(PAG_GPU_EINVAL, "null argument");
+        if (nn >= 0xFFFFFFFFull) throw_err(PAG_GPU_EINVAL, "batch too large");
         for (uint64_t i = 0; i < nn; ++i)
             if (nodes[i] >= ix->n) throw_err(PAG_GPU_EINVAL, "node id out of range");
         const size_t nd = ix->reps.size();
         std::vector<uint32_t> status(nd, 0);
-        std::vector<PagError> errs;
-        std::mutex emu;
-        auto shard = [&](size_t d) {
-            const uint64_t q0 = nn * d / nd, q1 = nn * (d + 1) / nd;
+        run_replicas(*ix, [&](size_t d) {
+            const uint64_t q0 = shard_lo(nn, d, nd), q1 = shard_lo(nn, d + 1, nd);
             ConstructionHost ch{nodes + q0, pes_on, pes_cap, pes ? pes + q0 * pes_cap : nullptr, pes_n + q0};
-            try {
-                search_on_replica(*ix, ix->reps[d], p, nullptr, q1 - q0, ids + q0 * p.K, sq + q0 * p.K,
-                                  n_out + q0, stats ? stats + q0 : nullptr, &status[d], &ch);
-            } catch (const PagError& e) {
-                std::lock_guard<std::mutex> lk(emu);
-                errs.push_back(e);
-            }
-        };
-        if (nd == 1) {
-            shard(0);
-        } else {
-            std::vector<std::thread> th;
-            for (size_t d = 0; d < nd; ++d) th.emplace_back(shard, d);
-            for (auto& t : th) t.join();
-        }
-        if (!errs.empty()) throw errs.front();
-        uint32_t so = 0;
-        for (auto s : status) so |= s;
-        if (so & pagdev::kStatusVisitedOverflow)
-            throw_err(PAG_GPU_ERUNTIME, "visited set overflow after retries");
+            search_on_replica(*ix, ix->reps[d], p, nullptr, q1 - q0, ids + q0 * p.K, sq + q0 * p.K, n_out + q0,
+                              stats ? stats + q0 : nullptr, &status[d], &ch);
+        });
     });
 }
 
@@ -1538,14 +1668,7 @@ int pag_gpu_construction_search_device(pag_gpu_index* ix, const uint32_t* nodes_
     return guarded([&] {
         if (!ix) throw_err(PAG_GPU_EINVAL, "null argument");
         std::lock_guard<std::mutex> g(ix->mu);
-        pag_search_params p{};
-        if (params) {
-            p = *params;
-        } else {
-            pag_gpu_default_params(&p);
-            p.K = p.efS = ix->efC;
-            p.b_override = ix->b_build;
-        }
+        const pag_search_params p = construction_params(*ix, params);
         validate_params(*ix, p);
         if (nn >= 0xFFFFFFFFull) throw_err(PAG_GPU_EINVAL, "batch too large");
         Replica& r = ix->reps[0];
@@ -1556,8 +1679,8 @@ int pag_gpu_construction_search_device(pag_gpu_index* ix, const uint32_t* nodes_
         ca.pes_cap = pes_cap;
         ca.pes = pes_dev;
         ca.pes_n = pes_n_dev;
-        run_search(*ix, r, p, nullptr, static_cast<uint32_t>(nn), nullptr, ids_dev, sq_dev, n_out_dev, stats_dev,
-                   static_cast<cudaStream_t>(stream), 0, &ca);
+        run_search(*ix, r, p, nullptr, static_cast<uint32_t>(nn), ids_dev, sq_dev, n_out_dev, stats_dev,
+                   static_cast<cudaStream_t>(stream), &ca);
     });
 }
 
@@ -1571,15 +1694,13 @@ int pag_gpu_search_submit(pag_gpu_index* ix, const float* q, uint64_t nq, const 
         if (nq && (!q || !n_out || (p.K && (!ids || !sq)))) throw_err(PAG_GPU_EINVAL, "null argument");
         if (nq >= 0xFFFFFFFFull) throw_err(PAG_GPU_EINVAL, "batch too large");
         const uint64_t t = ++ix->async_seq;
-        *ticket = t;
         const size_t nd = ix->reps.size();
-        uint32_t so = 0;
-        for (size_t d = 0; d < nd; ++d) {
-            const uint64_t q0 = nq * d / nd, q1 = nq * (d + 1) / nd;
+        submit_all(*ix, t, [&](size_t d) {
+            const uint64_t q0 = shard_lo(nq, d, nd), q1 = shard_lo(nq, d + 1, nd);
             async_submit_replica(*ix, ix->reps[d], p, q + q0 * ix->dim, q1 - q0, ids + q0 * p.K, sq + q0 * p.K,
-                                 n_out + q0, stats ? stats + q0 : nullptr, t, &so);
-        }
-        check_status(so);  // (from an older batch completed to free its slot)
+                                 n_out + q0, stats ? stats + q0 : nullptr, t);
+        });
+        *ticket = t;
     });
 }
 
@@ -1590,14 +1711,7 @@ int pag_gpu_construction_submit(pag_gpu_index* ix, const uint32_t* nodes, uint64
     return guarded([&] {
         if (!ix || !ticket) throw_err(PAG_GPU_EINVAL, "null argument");
         std::lock_guard<std::mutex> g(ix->mu);
-        pag_search_params p{};
-        if (params) {
-            p = *params;
-        } else {  // insert_with_state (builder.cpp:220-224)
-            pag_gpu_default_params(&p);
-            p.K = p.efS = ix->efC;
-            p.b_override = ix->b_build;
-        }
+        const pag_search_params p = construction_params(*ix, params);
         const uint32_t pes_on = collect_pes < 0 ? ix->enable_pes : static_cast<uint32_t>(collect_pes != 0);
         validate_params(*ix, p);
         if (nn && (!nodes || !n_out || !pes_n || (p.K && (!ids || !sq)) || (pes_cap && !pes)))
@@ -1606,16 +1720,14 @@ int pag_gpu_construction_submit(pag_gpu_index* ix, const uint32_t* nodes, uint64
         for (uint64_t i = 0; i < nn; ++i)
             if (nodes[i] >= ix->n) throw_err(PAG_GPU_EINVAL, "node id out of range");
         const uint64_t t = ++ix->async_seq;
-        *ticket = t;
         const size_t nd = ix->reps.size();
-        uint32_t so = 0;
-        for (size_t d = 0; d < nd; ++d) {
-            const uint64_t q0 = nn * d / nd, q1 = nn * (d + 1) / nd;
+        submit_all(*ix, t, [&](size_t d) {
+            const uint64_t q0 = shard_lo(nn, d, nd), q1 = shard_lo(nn, d + 1, nd);
             ConstructionHost ch{nodes + q0, pes_on, pes_cap, pes ? pes + q0 * pes_cap : nullptr, pes_n + q0};
             async_submit_replica(*ix, ix->reps[d], p, nullptr, q1 - q0, ids + q0 * p.K, sq + q0 * p.K, n_out + q0,
-                                 stats ? stats + q0 : nullptr, t, &so, &ch);
-        }
-        check_status(so);
+                                 stats ? stats + q0 : nullptr, t, &ch);
+        });
+        *ticket = t;
     });
 }
 
@@ -1625,13 +1737,24 @@ int pag_gpu_search_wait(pag_gpu_index* ix, uint64_t ticket) {
         std::lock_guard<std::mutex> g(ix->mu);
         if (ticket == 0 || ticket > ix->async_seq) throw_err(PAG_GPU_EINVAL, "unknown ticket");
         uint32_t so = 0;
+        auto it = ix->early_status.find(ticket);  // completed by a later submit
+        if (it != ix->early_status.end()) {
+            so |= it->second;
+            ix->early_status.erase(it);
+        }
+        std::exception_ptr first;
         for (auto& r : ix->reps) {
             Replica::AsyncSlot& a = r.aslot[ticket % Replica::kAsyncDepth];
             if (a.ticket == ticket) {
-                cuda_check(cudaSetDevice(r.device), "cudaSetDevice");
-                async_complete(*ix, r, a, &so);
+                try {
+                    cuda_check(cudaSetDevice(r.device), "cudaSetDevice");
+                    async_complete(r, a, &so);
+                } catch (...) {
+                    if (!first) first = std::current_exception();
+                }
             }
         }
+        if (first) std::rethrow_exception(first);
         check_status(so);
     });
 }
@@ -1648,8 +1771,7 @@ int pag_gpu_search_device(pag_gpu_index* ix, const float* q_dev, uint64_t nq,
         cuda_check(cudaSetDevice(r.device), "cudaSetDevice");
         cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
         if (nq >= 0xFFFFFFFFull) throw_err(PAG_GPU_EINVAL, "batch too large");
-        run_search(*ix, r, p, q_dev, static_cast<uint32_t>(nq), nullptr, ids_dev, sq_dev, n_out_dev,
-                   stats_dev, s, 0);
+        run_search(*ix, r, p, q_dev, static_cast<uint32_t>(nq), ids_dev, sq_dev, n_out_dev, stats_dev, s);
     });
 }
 
@@ -1661,26 +1783,13 @@ int pag_gpu_ground_truth(pag_gpu_index* ix, const float* queries, uint64_t nq, u
         if (nq == 0 || k == 0) return;
         if (!queries || !ids || !sq) throw_err(PAG_GPU_EINVAL, "null argument");
         const size_t nd = ix->reps.size();
-        std::vector<PagError> errs;
-        std::mutex emu;
-        auto shard = [&](size_t d) {
-            const uint64_t q0 = nq * d / nd, q1 = nq * (d + 1) / nd;
-            try {
-                ground_truth_on_replica(*ix, ix->reps[d], queries + q0 * ix->dim, q1 - q0, k,
-                                        ids + q0 * k, sq + q0 * k);
-            } catch (const PagError& e) {
-                std::lock_guard<std::mutex> lk(emu);
-                errs.push_back(e);
-            }
-        };
-        if (nd == 1) {
-            shard(0);
-        } else {
-            std::vector<std::thread> th;
-            for (size_t d = 0; d < nd; ++d) th.emplace_back(shard, d);
-            for (auto& t : th) t.join();
-        }
-        if (!errs.empty()) throw errs.front();
+        std::vector<uint64_t> unc(nd, 0);
+        run_replicas(*ix, [&](size_t d) {
+            const uint64_t q0 = shard_lo(nq, d, nd), q1 = shard_lo(nq, d + 1, nd);
+            unc[d] = ground_truth_on_replica(*ix, ix->reps[d], queries + q0 * ix->dim, q1 - q0, k, ids + q0 * k,
+                                             sq + q0 * k);
+        });
+        for (auto u : unc) ix->gt_uncertified += u;
     });
 }
 
@@ -1689,6 +1798,6 @@ const char* pag_gpu_last_error(void) { return g_err.c_str(); }
 // diagnostic (PAG_PHASE_TIMING builds): per-phase summed warp cycles
 void pag_gpu_phase_cycles(unsigned long long* out8, int reset) { pagdev::search_phase_cycles(out8, reset != 0); }
 
-const char* pag_gpu_version(void) { return "pag_gpu 0.1 (sm_100a)"; }
+const char* pag_gpu_version(void) { return "pag_gpu 0.2 (sm_100a)"; }
 
 }  // extern "C"

@@ -143,7 +143,7 @@ struct Common {
     uint32_t hs_log2, hs_count, hs_limit;  // marks held on chip before the bitmap takes over
     uint32_t* gbm;
     uint32_t gbm_words, gt_count;
-    bool gt_used, overflow;
+    bool gt_used;
     // R_L (routing.hpp:150, capacity efS) is never read during the search:
     // flushed W entries are appended here and the cap-limited sorted list is
     // formed once at the end (the bounded insert keeps the efS smallest, an
@@ -1667,37 +1667,31 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
     // start while the previous search launch on the stream drains its last
     // queries. Everything before a warp's first output write only reads the
     // index and this launch's own counter/scratch set; before that write the
-    // warp waits for the predecessor to complete, zeroes the predecessor's
-    // counter (the next launch's), and lets the next launch be scheduled.
+    // warp waits for the predecessor to complete and lets the next launch be
+    // scheduled (whose counter and scratch set are the predecessor's).
     bool released = false;
     auto release = [&]() {
         if (released) return;
         released = true;
         asm volatile("griddepcontrol.wait;" ::: "memory");
-        if (blockIdx.x == 0 && lane == 0) {
-            *P.qcounter_other = 0u;
-            __threadfence();
-        }
-        __syncwarp();
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     };
 
     while (true) {
         uint32_t qi = 0;
-        if (lane == 0) qi = atomicAdd(P.qcounter, 1u);
+        if (lane == 0) qi = atomicAdd(P.qcounter, 1u) - P.qbase;  // (mod 2^32, see SearchLaunch::qbase)
         qi = __shfl_sync(FULL, qi, 0);
-        if (qi >= P.nq) {
+        if (qi >= P.nq) {  // each warp draws exactly one index >= nq
             release();
             break;
         }
-        const uint32_t qid = P.qlist ? P.qlist[qi] : qi;
+        const uint32_t qid = qi;
 
         // ---- reset (routing.cpp:12-30)
         c.rl_size = 0;
         c.hs_count = 0;
         c.gt_count = 0;
         c.gt_used = false;
-        c.overflow = false;
         c.n_exact = c.n_test = c.n_pass = c.n_visited = c.n_edges = c.n_pes = 0;
         s.reset();
         for (uint32_t i = lane; i < (1u << c.hs_log2) / 4; i += 32)
@@ -1815,7 +1809,7 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
             __syncwarp();
         }
         // entry lists longer than 64 (b > 64 and n_entries > 64): remaining seeds
-        for (uint32_t e0 = 64; e0 < ix.n_entries && s.wsize < P.b && !c.overflow; e0 += 32) {
+        for (uint32_t e0 = 64; e0 < ix.n_entries && s.wsize < P.b; e0 += 32) {
             uint32_t sel = 0, myid = 0, room = P.b - s.wsize;
             for (uint32_t t = 0; t < 32 && e0 + t < ix.n_entries && room; ++t) {
                 const uint32_t id = __ldg(ix.entries + e0 + t);
@@ -1839,8 +1833,8 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
 
         PT(0);
         // ---- rounds (routing.cpp:229-240)
-        for (uint32_t r = 0; r < P.r_max && !c.overflow; ++r) {
-            while (!c.overflow) {
+        for (uint32_t r = 0; r < P.r_max; ++r) {
+            while (true) {
                 const uint32_t i = s.next_unvisited(lane);
                 if (i == EMPTY) break;
                 const uint32_t u = PES ? s.entry_id(i) : 0u;
@@ -1878,7 +1872,7 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
             st[kStatPass] = c.n_pass;
             st[kStatVisited] = c.n_visited;
             st[kStatEdges] = c.n_edges;
-            st[kStatStatus] = c.overflow ? kStatusVisitedOverflow : 0u;
+            st[kStatStatus] = 0u;
             st[6] = c.hs_count + c.gt_count;  // marks held
             st[7] = c.gt_count;               // of which in the HBM bitmap
             if (P.out_pes_n) P.out_pes_n[qid] = c.n_pes;
@@ -1917,7 +1911,7 @@ cudaError_t launch_t(const SearchLaunch& L, int grid, size_t smem, cudaStream_t 
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     static const int pdl = std::getenv("PAG_GPU_NO_PDL") ? 0 : 1;
-    attr[0].val.programmaticStreamSerializationAllowed = pdl;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl && L.pdl;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, k, L);

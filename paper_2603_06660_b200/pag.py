@@ -90,10 +90,19 @@ class PendingBatch:
 
     def wait(self) -> BatchResult:
         if not self._done:
-            check(lib.pag_gpu_search_wait(self._index.handle, self.ticket))
-            self._done = True
+            self._done = True  # the slot is released even when the batch failed
             self._q = None
+            check(lib.pag_gpu_search_wait(self._index.handle, self.ticket))
         return self._res
+
+    def __del__(self):
+        # the kernel writes into pinned memory that is unpacked into this
+        # batch's arrays at completion: never drop them before that
+        if not getattr(self, "_done", True):
+            try:
+                self.wait()
+            except Exception:
+                pass
 
 
 @dataclass
@@ -114,11 +123,13 @@ class PagIndex:
     reference, builder.hpp:62-69; here a handle released by close())."""
 
     def __init__(self, path: str, devices: Sequence[int] = (0,)):
-        mask = 0
-        for d in devices:
-            mask |= 1 << int(d)
+        """One replica per entry of `devices` (CUDA device ordinals; an entry
+        may repeat, giving several replicas on one GPU). Batches are split
+        into contiguous shards, one per replica (pag_gpu_open_devices)."""
+        devs = [int(d) for d in devices] or [0]
+        arr = (C.c_int * len(devs))(*devs)
         self._h = C.c_void_p()
-        check(lib.pag_gpu_open(path.encode(), mask, C.byref(self._h)))
+        check(lib.pag_gpu_open_devices(path.encode(), arr, len(devs), C.byref(self._h)))
         info = np.zeros(16, np.uint64)
         check(lib.pag_gpu_info(self._h, info, 16))
         (self.n, self.dim, self.padded_dim, self.L, self.m, self.M, metric, self.n_entries,
