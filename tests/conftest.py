@@ -54,6 +54,13 @@ FIXTURES = {
                 dict(M=16, efC=100, seed=15)),
     "unit1024": (dict(n=1000, d=1024, centres=16, sigma=0.3, unit=True, metric="euclidean"),
                  dict(M=16, efC=100, seed=17)),
+    # dim % L != 0: queries and rows zero-padded to padded_dim (routing.cpp:253-254)
+    # d=30 -> L=4, padded 32 (dstride 32)
+    "pad30": (dict(n=1800, d=30, centres=15, sigma=0.5, unit=False, metric="euclidean"),
+              dict(M=12, efC=80, seed=19)),
+    # d=9 -> L=2, padded 10, dstride 12; cosine (normalisation after padding)
+    "pad9c": (dict(n=1400, d=9, centres=12, sigma=0.5, unit=False, metric="cosine"),
+              dict(M=8, efC=60, seed=21)),
 }
 
 

@@ -22,6 +22,8 @@ CASES = [
     ("euc48", 10, 10), ("euc48", 10, 40), ("euc48", 10, 200), ("euc48", 1, 1), ("euc48", 32, 64),
     ("euc48", 100, 300), ("cos20", 10, 50), ("cos20", 5, 5), ("tail10", 10, 30), ("tail10", 40, 90),
     ("deg64", 10, 60), ("deg64", 64, 128),
+    # dim % L != 0 (zero padding of queries and rows, routing.cpp:253-254)
+    ("pad30", 10, 40), ("pad30", 50, 120), ("pad9c", 10, 30), ("pad9c", 33, 70),
 ]
 
 
@@ -51,7 +53,7 @@ def test_oracle_ablations_match_reference(built, fixture_dir, flags):
         assert np.array_equal(got[3][:, 1], got[3][:, 2])
 
 
-@pytest.mark.parametrize("name", ["euc48", "cos20", "tail10"])
+@pytest.mark.parametrize("name", ["euc48", "cos20", "tail10", "pad30", "pad9c"])
 def test_tables_and_refs_match_reference(built, fixture_dir, name):
     fx = built(name)
     ix = O.OracleIndex(fx["index"])
