@@ -154,6 +154,34 @@ struct GtTcLaunch {
 };
 cudaError_t launch_gt_tc(const GtTcLaunch& g, cudaStream_t stream);
 
+// Tensor-core ground truth for 32 < k <= 1000 (pag_gt_tc.cu): per-query
+// distance bound from k search-result rows, TF32 tcgen05 GEMM whose epilogue
+// appends the rows under the bound to the query's pool, exact re-rank of the
+// pool. Queries whose pool overflowed are flagged for the exact re-run.
+struct GtTcPoolLaunch {
+    const void* tmA;  // CUtensorMap over queries (nq x padded, row pitch dstride*4)
+    const void* tmB;  // CUtensorMap over base rows (n x padded)
+    const float* base;
+    uint64_t n;
+    uint32_t padded, dstride;
+    const float* queries;       // nq x dstride, zero padded
+    uint32_t nq, k, nsplit;
+    uint64_t rows_per_split;    // multiple of gt_tc_block_n()
+    float* qnorm;               // nq scratch
+    const float* bnorm;         // n squared base norms
+    float max_bnorm;
+    const uint32_t* search_ids; // nq x k: rows of a graph search of each query (any k distinct rows)
+    const uint32_t* search_n;   // nq: valid entries (< k: the query is re-run exactly)
+    float* thrx;                // nq scratch: filter bound
+    uint32_t* pool_cnt;         // nq
+    uint32_t* pool_id;          // nq x pool_cap
+    uint32_t pool_cap;          // <= 8192
+    uint32_t* out_ids;          // nq x k
+    float* out_sq;              // nq x k
+    uint32_t* uncertified;      // nq flags: 1 = re-run exactly
+};
+cudaError_t launch_gt_tc_pool(const GtTcPoolLaunch& g, cudaStream_t stream);
+
 // pag_util.cu: staged node blocks -> their slots in the adjacency array
 cudaError_t scatter_blocks(const void* staging, const uint32_t* ids, uint32_t count, void* adj,
                            uint32_t block_bytes, cudaStream_t stream);

@@ -16,9 +16,22 @@
 //      result is exact when the k-th exact distance is below the smallest
 //      excluded approximate distance minus 2*delta. Uncertified queries are
 //      re-run by the exact SIMT kernel (pag_gt.cu) on the host's request.
+//
+// Large k (32 < k <= 1000, the K = 100 / 1000 configs): a per-query distance
+// bound replaces the per-split top-C lists. T_q = the largest exact distance
+// of any k distinct rows (the host takes the k ids of a graph search of the
+// query: a search only supplies rows, never results) bounds the k-th true
+// distance from above, so the true top-k lies among the rows whose
+// approximate distance is <= T_q + delta. The GEMM epilogue is then a pure
+// filter (packed FFMA2 + 3-input min over 32 columns, a warp vote, and an
+// atomic append to the query's pool for the rare passes); the re-rank takes
+// the exact distances of the pool, sorts by (sq, id) and keeps k. A pool that
+// overflows (or a query without k search results) is re-run exactly.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <type_traits>
 
 #include "pag_device.h"
 
@@ -127,13 +140,35 @@ struct TcSmem {
     uint32_t tmem_base;
 };
 
+// smem of the threshold-filter flavour (no per-row candidate lists)
+struct TcSmemF {
+    uint8_t stage[STAGES][STAGE_BYTES];
+    float bnorm[2][BN];
+    uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+    uint32_t tmem_base;
+};
+
+__device__ __forceinline__ float min3f(float a, float b, float c) {
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+// THRESH = false: per (query, split) the C nearest approximate candidates
+// (cand_d / cand_id / cand_thr). THRESH = true: every row whose approximate
+// x = |b|^2 - 2 q.b is below the query's bound thrx[q] is appended to the
+// query's pool (pool_id[q * pool_cap + slot], slot from atomicAdd on
+// pool_cnt[q]; slots past pool_cap are counted, not written).
+template <bool THRESH>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gt_tc_candidates(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const float* __restrict__ qnorm, const float* __restrict__ bnorm, uint32_t nq, uint64_t n,
                      uint32_t kblocks, uint64_t rows_per_split, uint32_t C, float* __restrict__ cand_d,
-                     uint32_t* __restrict__ cand_id, float* __restrict__ cand_thr) {
+                     uint32_t* __restrict__ cand_id, float* __restrict__ cand_thr, const float* __restrict__ thrx,
+                     uint32_t* __restrict__ pool_cnt, uint32_t* __restrict__ pool_id, uint32_t pool_cap) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    TcSmem& sm = *reinterpret_cast<TcSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    using Sm = typename std::conditional<THRESH, TcSmemF, TcSmem>::type;
+    Sm& sm = *reinterpret_cast<Sm*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t m0 = blockIdx.x * BM;
     const uint32_t split = blockIdx.y, nsplit = gridDim.y;
@@ -218,6 +253,57 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t row = quarter * 32 + lane;
         const uint32_t qi = m0 + row;
         const bool valid_q = qi < nq;
+        if constexpr (THRESH) {
+            // x = |b|^2 - 2 q.b (the approximate distance minus |q|^2), two
+            // columns per FFMA2; a 32-column chunk is skipped by the warp when
+            // no lane's minimum is below its bound (almost always)
+            const float thr = valid_q ? thrx[qi] : -PAG_INF;
+            for (uint32_t t = 0; t < ntiles; ++t) {
+                const uint32_t as = t & 1u, aph = (t >> 1) & 1u;
+                const uint64_t c0 = r0 + static_cast<uint64_t>(t) * BN;
+                const uint32_t et = ew * 32 + lane;
+                for (uint32_t j = et; j < BN; j += 128)
+                    sm.bnorm[as][j] = (c0 + j < r1) ? bnorm[c0 + j] : PAG_INF;
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                mbar_wait(&sm.tfull[as], aph);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+                for (int ch = 0; ch < BN / 32; ++ch) {
+                    float v[32];
+                    tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + as * BN + ch * 32, v);
+                    float x[32];
+                    const float2* bn2 = reinterpret_cast<const float2*>(&sm.bnorm[as][ch * 32]);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const float2 r = __ffma2_rn(make_float2(v[2 * i], v[2 * i + 1]), make_float2(-2.0f, -2.0f),
+                                                    bn2[i]);
+                        x[2 * i] = r.x;
+                        x[2 * i + 1] = r.y;
+                    }
+                    float m[11];
+#pragma unroll
+                    for (int i = 0; i < 10; ++i) m[i] = min3f(x[3 * i], x[3 * i + 1], x[3 * i + 2]);
+                    m[10] = fminf(x[30], x[31]);
+                    const float mm = min3f(min3f(m[0], m[1], m[2]), min3f(m[3], m[4], m[5]),
+                                           min3f(min3f(m[6], m[7], m[8]), m[9], m[10]));
+                    const bool hit = mm < thr;
+                    if (__any_sync(0xffffffffu, hit)) {
+                        if (hit) {
+#pragma unroll
+                            for (int i = 0; i < 32; ++i)
+                                if (x[i] < thr) {
+                                    const uint32_t slot = atomicAdd(pool_cnt + qi, 1u);
+                                    if (slot < pool_cap)
+                                        pool_id[static_cast<uint64_t>(qi) * pool_cap + slot] =
+                                            static_cast<uint32_t>(c0 + ch * 32 + i);
+                                }
+                        }
+                    }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                mbar_arrive(&sm.tempty[as]);
+            }
+        } else {
         const float qn = valid_q ? qnorm[qi] : 0.0f;
         uint32_t cnt = 0, max_i = 0;
         float max_v = PAG_INF;
@@ -280,6 +366,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             // every excluded row of this split has approx >= thr
             cand_thr[static_cast<uint64_t>(qi) * nsplit + split] = cnt == C ? max_v : PAG_INF;
         }
+        }  // !THRESH
     }
     __syncthreads();
     if (warp == 1) {
@@ -385,22 +472,129 @@ __global__ void __launch_bounds__(256) gt_tc_rerank(const float* __restrict__ ba
     }
 }
 
+// one warp per query: T = the largest exact distance of the query's k
+// search-result rows (any k distinct rows bound the k-th true distance from
+// above), then the filter bound in the epilogue's x space, with 2 delta of
+// slack: every row whose exact distance is <= T has x < thrx (|approx -
+// exact| <= delta, rounding of x and of thrx far below delta)
+__global__ void gt_tc_bound(const float* __restrict__ base, uint32_t dstride, uint32_t D,
+                            const float* __restrict__ queries, const float* __restrict__ qnorm, float max_bnorm,
+                            uint32_t nq, uint32_t k, const uint32_t* __restrict__ s_ids,
+                            const uint32_t* __restrict__ s_n, float* __restrict__ thrx) {
+    const uint32_t qi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (qi >= nq) return;
+    const float* q = queries + static_cast<uint64_t>(qi) * dstride;
+    float t = 0.0f;
+    const bool ok = s_n[qi] >= k;
+    if (ok)
+        for (uint32_t i = lane; i < k; i += 32)
+            t = fmaxf(t, sq_dist_ref(base + static_cast<uint64_t>(s_ids[static_cast<uint64_t>(qi) * k + i]) * dstride,
+                                     q, D));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, o));
+    if (lane == 0) {
+        const float qn = qnorm[qi];
+        const float delta = 0.0078125f * sqrtf(qn) * sqrtf(max_bnorm) + 1e-5f * (qn + max_bnorm) + 1e-30f;
+        thrx[qi] = ok ? (t - qn) + 2.0f * delta : -PAG_INF;  // -inf: no pool, the host re-runs the query
+    }
+}
+
+// one CTA per query: exact reference-order distances of the pool, bitonic
+// sort by (sq, id), top-k out; a pool that overflowed or holds fewer than k
+// rows marks the query for the exact re-run
+__global__ void __launch_bounds__(256) gt_tc_rerank_pool(const float* __restrict__ base, uint32_t dstride,
+                                                         uint32_t D, const float* __restrict__ queries,
+                                                         const uint32_t* __restrict__ pool_cnt,
+                                                         const uint32_t* __restrict__ pool_id, uint32_t cap, uint32_t k,
+                                                         uint32_t* __restrict__ out_ids, float* __restrict__ out_sq,
+                                                         uint32_t* __restrict__ uncertified) {
+    extern __shared__ __align__(16) uint64_t keys[];
+    const uint32_t qi = blockIdx.x;
+    const uint32_t cnt = pool_cnt[qi];
+    if (cnt > cap || cnt < k) {
+        if (threadIdx.x == 0) uncertified[qi] = 1u;
+        return;
+    }
+    uint32_t p = 1;
+    while (p < cnt) p <<= 1;
+    const float* q = queries + static_cast<uint64_t>(qi) * dstride;
+    for (uint32_t i = threadIdx.x; i < p; i += blockDim.x) {
+        uint64_t key = ~0ull;
+        if (i < cnt) {
+            const uint32_t id = pool_id[static_cast<uint64_t>(qi) * cap + i];
+            const float s = sq_dist_ref(base + static_cast<uint64_t>(id) * dstride, q, D);
+            key = (static_cast<uint64_t>(__float_as_uint(s)) << 32) | id;
+        }
+        keys[i] = key;
+    }
+    __syncthreads();
+    for (uint32_t size = 2; size <= p; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t t = threadIdx.x; t < p / 2; t += blockDim.x) {
+                const uint32_t lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const uint64_t a = keys[lo], b = keys[hi];
+                if ((a > b) == up) {
+                    keys[lo] = b;
+                    keys[hi] = a;
+                }
+            }
+            __syncthreads();
+        }
+    for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
+        const uint64_t key = keys[i];
+        out_ids[static_cast<uint64_t>(qi) * k + i] = static_cast<uint32_t>(key);
+        out_sq[static_cast<uint64_t>(qi) * k + i] = __uint_as_float(static_cast<uint32_t>(key >> 32));
+    }
+    if (threadIdx.x == 0) uncertified[qi] = 0u;
+}
+
 }  // namespace
 
 size_t gt_tc_smem_bytes() { return sizeof(TcSmem) + 1024; }
 
+cudaError_t launch_gt_tc_pool(const GtTcPoolLaunch& g, cudaStream_t stream) {
+    cudaError_t e;
+    const size_t smem = sizeof(TcSmemF) + 1024;
+    e = cudaFuncSetAttribute(gt_tc_candidates<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    row_sqnorm<<<static_cast<unsigned>((g.nq * 32ull + 255) / 256), 256, 0, stream>>>(g.queries, g.nq, g.dstride,
+                                                                                     g.padded, g.qnorm);
+    gt_tc_bound<<<static_cast<unsigned>((g.nq * 32ull + 255) / 256), 256, 0, stream>>>(
+        g.base, g.dstride, g.padded, g.queries, g.qnorm, g.max_bnorm, g.nq, g.k, g.search_ids, g.search_n, g.thrx);
+    e = cudaMemsetAsync(g.pool_cnt, 0, 4ull * g.nq, stream);
+    if (e != cudaSuccess) return e;
+    dim3 grid((g.nq + BM - 1) / BM, g.nsplit);
+    gt_tc_candidates<true><<<grid, TC_THREADS, smem, stream>>>(
+        *static_cast<const CUtensorMap*>(g.tmA), *static_cast<const CUtensorMap*>(g.tmB), g.qnorm, g.bnorm, g.nq, g.n,
+        (g.padded + BK - 1) / BK, g.rows_per_split, 0, nullptr, nullptr, nullptr, g.thrx, g.pool_cnt, g.pool_id,
+        g.pool_cap);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    uint32_t p = 1;
+    while (p < g.pool_cap) p <<= 1;
+    e = cudaFuncSetAttribute(gt_tc_rerank_pool, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p * 8));
+    if (e != cudaSuccess) return e;
+    gt_tc_rerank_pool<<<g.nq, 256, p * 8, stream>>>(g.base, g.dstride, g.padded, g.queries, g.pool_cnt, g.pool_id,
+                                                    g.pool_cap, g.k, g.out_ids, g.out_sq, g.uncertified);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_gt_tc(const GtTcLaunch& g, cudaStream_t stream) {
     cudaError_t e;
     const size_t smem = gt_tc_smem_bytes();
-    e = cudaFuncSetAttribute(gt_tc_candidates, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    e = cudaFuncSetAttribute(gt_tc_candidates<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     row_sqnorm<<<static_cast<unsigned>((g.nq * 32ull + 255) / 256), 256, 0, stream>>>(g.queries, g.nq, g.dstride,
                                                                                      g.padded, g.qnorm);
     dim3 grid((g.nq + BM - 1) / BM, g.nsplit);
-    gt_tc_candidates<<<grid, TC_THREADS, smem, stream>>>(*static_cast<const CUtensorMap*>(g.tmA),
-                                                         *static_cast<const CUtensorMap*>(g.tmB), g.qnorm, g.bnorm,
-                                                         g.nq, g.n, (g.padded + BK - 1) / BK, g.rows_per_split,
-                                                         g.C, g.cand_d, g.cand_id, g.cand_thr);
+    gt_tc_candidates<false><<<grid, TC_THREADS, smem, stream>>>(
+        *static_cast<const CUtensorMap*>(g.tmA), *static_cast<const CUtensorMap*>(g.tmB), g.qnorm, g.bnorm, g.nq, g.n,
+        (g.padded + BK - 1) / BK, g.rows_per_split, g.C, g.cand_d, g.cand_id, g.cand_thr, nullptr, nullptr, nullptr,
+        0);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     uint32_t p = 1;

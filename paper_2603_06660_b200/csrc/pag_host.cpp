@@ -1026,9 +1026,69 @@ uint64_t ground_truth_on_replica(pag_gpu_index& ix, Replica& r, const float* q, 
     for (uint64_t i = 0; i < nq; ++i) std::memcpy(&qp[i * ix.dstride], q + i * ix.dim, 4ull * ix.dim);
     DevBuf d_q(4 * qp.size()), d_ids(4ull * nq * kk), d_sq(4ull * nq * kk);
     cuda_check(cudaMemcpy(d_q.p, qp.data(), 4 * qp.size(), cudaMemcpyHostToDevice), "H2D");
-    const bool tc = kk <= pagdev::gt_tc_cmax() / 2 && r.bnorm && !std::getenv("PAG_GPU_GT_EXACT");
+    const bool no_tc = !r.bnorm || std::getenv("PAG_GPU_GT_EXACT");
+    // k <= 32: per-split top-C lists; 32 < k <= 1000 (or PAG_GPU_GT_POOL set):
+    // per-query bound + pool; otherwise the exact SIMT kernel
+    const bool pool = !no_tc && kk <= 1000 && (kk > pagdev::gt_tc_cmax() / 2 || std::getenv("PAG_GPU_GT_POOL"));
+    const bool tc = !no_tc && !pool && kk <= pagdev::gt_tc_cmax() / 2;
     std::vector<uint32_t> redo;
-    if (tc) {
+    if (pool) {
+        // 1. k rows per query from a graph search of the raw query (ids only;
+        //    any k distinct rows give the bound)
+        pag_search_params sp;
+        pag_gpu_default_params(&sp);
+        sp.K = sp.efS = kk;
+        sp.exact_dist = 0;
+        DevBuf rawq(4ull * nq * ix.dim), sids(4ull * nq * kk), ssq(4ull * nq * kk), sn(4ull * nq),
+            sst(4ull * nq * pagdev::kStatWords);
+        cuda_check(cudaMemcpyAsync(rawq.p, q, 4ull * nq * ix.dim, cudaMemcpyHostToDevice, r.stream), "H2D");
+        run_search(ix, r, sp, rawq.as<float>(), nqu, sids.as<uint32_t>(), ssq.as<float>(), sn.as<uint32_t>(),
+                   sst.as<uint32_t>(), r.stream);
+        // 2. bound, filter GEMM into per-query pools, exact re-rank of the pools
+        const uint32_t BN = pagdev::gt_tc_block_n();
+        const uint32_t mt = (nqu + pagdev::gt_tc_block_m() - 1) / pagdev::gt_tc_block_m();
+        const uint64_t ntile = (ix.n + BN - 1) / BN;
+        uint32_t ns = std::max<uint32_t>(1, std::min<uint32_t>(64, (4u * r.num_sms + mt / 2) / mt));
+        const uint64_t rps = ((ntile + ns - 1) / ns) * BN;
+        ns = static_cast<uint32_t>((ix.n + rps - 1) / rps);
+        // pool capacity: the rows within 2 delta above the bound can be many
+        // more than k where the k-th neighbour lies in a dense shell (cfg-2
+        // k = 100: 35 of 10k queries overflowed 2048); 8192 x 4 B per query
+        const uint32_t cap = 8192;
+        CUtensorMap tmA = tensor_map_rows(d_q.as<float>(), nq, ix.padded, ix.dstride, pagdev::gt_tc_block_m());
+        CUtensorMap tmB = tensor_map_rows(r.rows, ix.n, ix.padded, ix.dstride, BN);
+        DevBuf qn(4ull * nq), thr(4ull * nq), pcnt(4ull * nq), pid(4ull * nq * cap), unc(4ull * nq);
+        pagdev::GtTcPoolLaunch g{};
+        g.tmA = &tmA;
+        g.tmB = &tmB;
+        g.base = r.rows;
+        g.n = ix.n;
+        g.padded = ix.padded;
+        g.dstride = ix.dstride;
+        g.queries = d_q.as<float>();
+        g.nq = nqu;
+        g.k = kk;
+        g.nsplit = ns;
+        g.rows_per_split = rps;
+        g.qnorm = qn.as<float>();
+        g.bnorm = r.bnorm;
+        g.max_bnorm = ix.max_bnorm;
+        g.search_ids = sids.as<uint32_t>();
+        g.search_n = sn.as<uint32_t>();
+        g.thrx = thr.as<float>();
+        g.pool_cnt = pcnt.as<uint32_t>();
+        g.pool_id = pid.as<uint32_t>();
+        g.pool_cap = cap;
+        g.out_ids = d_ids.as<uint32_t>();
+        g.out_sq = d_sq.as<float>();
+        g.uncertified = unc.as<uint32_t>();
+        cuda_check(pagdev::launch_gt_tc_pool(g, r.stream), "tensor-core ground truth (pool)");
+        std::vector<uint32_t> flags(nq);
+        cuda_check(cudaMemcpyAsync(flags.data(), unc.p, 4ull * nq, cudaMemcpyDeviceToHost, r.stream), "D2H");
+        cuda_check(cudaStreamSynchronize(r.stream), "tensor-core ground truth (pool)");
+        for (uint32_t i = 0; i < nqu; ++i)
+            if (flags[i]) redo.push_back(i);
+    } else if (tc) {
         const uint32_t C = pagdev::gt_tc_cmax(), BN = pagdev::gt_tc_block_n();
         const uint32_t mt = (nqu + pagdev::gt_tc_block_m() - 1) / pagdev::gt_tc_block_m();
         const uint64_t ntile = (ix.n + BN - 1) / BN;

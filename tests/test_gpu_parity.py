@@ -142,14 +142,24 @@ def test_ground_truth_bitexact(pag, built, name, k):
     assert np.array_equal(gi, oi) and np.array_equal(gs.view(np.uint32), os_.view(np.uint32))
 
 
-@pytest.mark.parametrize("name,k", [("euc48", 1), ("euc48", 10), ("euc48", 32), ("tail10", 16),
-                                    ("cos20", 8), ("deg64", 25)])
-def test_tensor_core_ground_truth_equals_exact(pag, built, monkeypatch, name, k):
-    """tcgen05 TF32 candidates + exact re-rank + certificate (k <= 32) gives
-    the same ids and bits as the exact SIMT kernel and the oracle."""
+@pytest.mark.parametrize("name,k,pool", [("euc48", 1, False), ("euc48", 10, False), ("euc48", 32, False),
+                                         ("tail10", 16, False), ("cos20", 8, False), ("deg64", 25, False),
+                                         ("euc48", 100, False), ("deg64", 1000, False), ("pad30", 200, False),
+                                         ("cos20", 64, False), ("unit512", 1000, False), ("euc48", 10, True),
+                                         ("pad9c", 5, True)])
+def test_tensor_core_ground_truth_equals_exact(pag, built, monkeypatch, name, k, pool):
+    """tcgen05 TF32 GEMM ground truth gives the same ids and bits as the exact
+    SIMT kernel and the oracle, with every query certified: k <= 32 by
+    per-split top-C candidates + certificate, 32 < k <= 1000 (and, forced,
+    small k) by the per-query bound + pool path."""
     fx = built(name)
     ix = gpu_index(pag, fx["index"])
+    if pool:
+        monkeypatch.setenv("PAG_GPU_GT_POOL", "1")
+    before = ix.gt_uncertified()
     ti, ts = ix.ground_truth(fx["queries"], k)
+    assert ix.gt_uncertified() == before, "tensor-core candidates not certified"
+    monkeypatch.delenv("PAG_GPU_GT_POOL", raising=False)
     monkeypatch.setenv("PAG_GPU_GT_EXACT", "1")
     ei, es = ix.ground_truth(fx["queries"], k)
     assert np.array_equal(ti, ei) and np.array_equal(ts.view(np.uint32), es.view(np.uint32))
