@@ -221,6 +221,7 @@ def compare_with_reference(g, r, K: int, gt_ids=None, gt_sq=None, tol: float = 1
     g_ids, g_sq, g_n, g_st = g_ids[:nq], g_sq[:nq], g_n[:nq], g_st[:nq]
     ids_eq = sq_eq = cnt_eq = sets_eq = 0
     unexplained, max_rel = 0, 0.0
+    examples = []
     for i in range(nq):
         gn, rn = int(g_n[i]), int(r_n[i])
         gi, ri = g_ids[i, :gn], r_ids[i, :rn]
@@ -241,9 +242,17 @@ def compare_with_reference(g, r, K: int, gt_ids=None, gt_sq=None, tol: float = 1
         diff = [gmap[k] for k in gmap.keys() - rmap.keys()] + [rmap[k] for k in rmap.keys() - gmap.keys()]
         if any(abs(x - kth) > tol * max(abs(kth), 1e-30) for x in diff):
             unexplained += 1
+            if len(examples) < 3:
+                examples.append({"query": i, "kth_sq": kth,
+                                 "gpu_only": sorted((float(gmap[k]), int(k)) for k in gmap.keys() - rmap.keys()),
+                                 "ref_only": sorted((float(rmap[k]), int(k)) for k in rmap.keys() - gmap.keys()),
+                                 "counters_gpu": [int(x) for x in np.asarray(g_st[i, :4])],
+                                 "counters_ref": [int(x) for x in np.asarray(r_st[i])]})
     out = {"queries": nq, "ids_equal": round(ids_eq / max(nq, 1), 5), "sq_bit_equal": round(sq_eq / max(nq, 1), 5),
            "counters_equal": round(cnt_eq / max(nq, 1), 5), "id_sets_equal": round(sets_eq / max(nq, 1), 5),
            "max_rel_sq_diff": float(max_rel), "unexplained_diffs": int(unexplained)}
+    if examples:
+        out["unexplained_examples"] = examples
     if gt_ids is not None:
         from paper_2603_06660_b200.recall import mean_recall
         rg = mean_recall(g_ids, g_n, gt_ids[:nq], gt_sq[:nq], K)
