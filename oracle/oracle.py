@@ -68,6 +68,7 @@ def lib():
         "pago_scalars": (C.POINTER(C.c_float), [P, C.c_uint32]),
         "pago_codes": (C.POINTER(C.c_uint8), [P, C.c_uint32]),
         "pago_row": (C.POINTER(C.c_float), [P, C.c_uint32]),
+        "pago_set_distance_mode": (None, [P, C.c_int]),
         "pago_search": (C.c_int, [P, f32p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                   C.c_int, C.c_int, u32p, f32p, u32p, u64p]),
         "pago_query_table": (C.c_int, [P, f32p, f32p]),
@@ -150,8 +151,21 @@ class OracleIndex:
     def degree(self, u: int) -> int:
         return int(lib().pago_degree(self._h, u))
 
+    def set_warp_tree(self, on: bool) -> None:
+        """Distances in the B200 library's warp-tree order (its exact_dist = 0
+        mode) instead of the reference order, for the search and the
+        construction search (pag_oracle.c warp_tree_sq_dist)."""
+        lib().pago_set_distance_mode(self._h, int(bool(on)))
+
     def search(self, queries: np.ndarray, K: int, efS: int, b_override: int = 0,
-               use_prt: bool = True, use_tfb: bool = True):
+               use_prt: bool = True, use_tfb: bool = True, warp_tree: bool = False):
+        self.set_warp_tree(warp_tree)
+        try:
+            return self._search(queries, K, efS, b_override, use_prt, use_tfb)
+        finally:
+            self.set_warp_tree(False)
+
+    def _search(self, queries, K, efS, b_override, use_prt, use_tfb):
         q = np.ascontiguousarray(queries, np.float32).reshape(-1, self.dim)
         nq = q.shape[0]
         ids = np.full((nq, max(K, 1)), 0xFFFFFFFF, np.uint32)
@@ -173,9 +187,16 @@ class OracleIndex:
         return ids, sq, n_out, stats
 
     def construction_search(self, nodes, K=None, efS=None, b_override=None, collect_pes=None,
-                            pes_cap: int = 256):
+                            pes_cap: int = 256, warp_tree: bool = False):
         """insert_with_state's search (builder.cpp:218-227) for existing nodes:
         returns (ids, sq, n_out, stats[nn,5], pes[nn,pes_cap], pes_n)."""
+        self.set_warp_tree(warp_tree)
+        try:
+            return self._construction_search(nodes, K, efS, b_override, collect_pes, pes_cap)
+        finally:
+            self.set_warp_tree(False)
+
+    def _construction_search(self, nodes, K, efS, b_override, collect_pes, pes_cap):
         nodes = np.ascontiguousarray(nodes, np.uint32).reshape(-1)
         K = self.efC if K is None else K
         efS = self.efC if efS is None else efS

@@ -302,7 +302,66 @@ struct pago_index {
     float* norms;        /* n */
     float* refs;         /* L * m * sub_dim */
     uint64_t total_edges;
+    int dist_mode;       /* 0: reference order (vecstore.cpp:77-95); 1: the B200 warp-tree order */
 };
+
+/* The B200 library's second distance mode (exact_dist = 0): FMA partials per
+ * lane over the float4s it loads, then a fixed xor-butterfly reduction
+ * (paper_2603_06660_b200/csrc/pag_search.cu, dist_fast_pairs / dist_fast).
+ * Restated here so that the GPU's warp-tree mode can be checked bit for bit
+ * too: the traversal logic is shared, so any difference between the two
+ * modes' results is attributable to the summation order alone. The GPU row
+ * stride is round_up(padded, 4); elements past padded are zero on both
+ * sides and contribute exact zeros. */
+static float warp_tree_sq_dist(const float* a, const float* q, uint32_t padded) {
+    const uint32_t ds = (padded + 3u) & ~3u;
+    const uint32_t nch = ds / 128u;
+    if (padded == ds && ds % 128u == 0 && (nch == 1 || nch == 4 || nch == 6 || nch == 8)) {
+        /* dist_fast_pairs<NCH>: 16 lanes, lane h owns float4 i at 64 i + 4 h */
+        float s[16];
+        for (uint32_t h = 0; h < 16; ++h) {
+            float ax = 0.0f, ay = 0.0f;
+            for (uint32_t i = 0; i < 2 * nch; ++i) {
+                const uint32_t k = 64u * i + 4u * h;
+                const float d0 = a[k] - q[k], d1 = a[k + 1] - q[k + 1], d2 = a[k + 2] - q[k + 2],
+                            d3 = a[k + 3] - q[k + 3];
+                ax = fmaf(d0, d0, ax);
+                ay = fmaf(d1, d1, ay);
+                ax = fmaf(d2, d2, ax);
+                ay = fmaf(d3, d3, ay);
+            }
+            s[h] = ax + ay;
+        }
+        for (uint32_t m = 8; m; m >>= 1)
+            for (uint32_t h = 0; h < m; ++h) s[h] = s[h] + s[h + m];
+        return s[0];
+    }
+    /* dist_fast<0>: 32 lanes, lane l owns float4 l of every 128-float chunk */
+    float p[32];
+    for (uint32_t l = 0; l < 32; ++l) {
+        float px = 0.0f, py = 0.0f;
+        for (uint32_t base = 0; base + 4u * l < ds; base += 128u) {
+            const uint32_t k = base + 4u * l;
+            float d[4];
+            for (uint32_t c = 0; c < 4; ++c) d[c] = k + c < padded ? a[k + c] - q[k + c] : 0.0f;
+            px = fmaf(d[0], d[0], px);
+            py = fmaf(d[1], d[1], py);
+            px = fmaf(d[2], d[2], px);
+            py = fmaf(d[3], d[3], py);
+        }
+        p[l] = px + py;
+    }
+    for (uint32_t m = 16; m; m >>= 1)
+        for (uint32_t l = 0; l < m; ++l) p[l] = p[l] + p[l + m];
+    return p[0];
+}
+
+static float row_dist(const struct pago_index* ix, uint32_t id, const float* q) {
+    const float* row = ix->rows + (size_t)id * ix->padded;
+    return ix->dist_mode ? warp_tree_sq_dist(row, q, ix->padded) : pago_sq_dist(row, q, ix->padded);
+}
+
+void pago_set_distance_mode(struct pago_index* ix, int mode) { ix->dist_mode = mode ? 1 : 0; }
 
 static int rd(FILE* f, void* p, size_t n) { return fread(p, 1, n, f) == n; }
 
@@ -706,7 +765,7 @@ static int expand_node(size_t work_idx, struct pago_tfb* st, const pago_index* i
             }
             if (pass) {
                 ++stats->pass;
-                float sq = pago_sq_dist(ix->rows + (size_t)w * ix->padded, q, ix->padded);
+                float sq = row_dist(ix, w, q);
                 ++stats->exact;
                 tfb_mark(st, w);
                 if (sq < tfb_admission_sq(st))
@@ -745,7 +804,7 @@ static int search_padded(const pago_index* ix, const float* q, uint32_t K, uint3
         uint32_t id = ix->entries[e];
         if (st->wsize >= b) break;
         if (id >= n || tfb_marked(st, id)) continue;
-        float s = pago_sq_dist(ix->rows + (size_t)id * ix->padded, q, ix->padded);
+        float s = row_dist(ix, id, q);
         ++stats->exact;
         tfb_mark(st, id);
         tfb_seed(st, id, s);

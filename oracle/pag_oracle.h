@@ -78,6 +78,10 @@ const float* pago_row(const pago_index* ix, uint32_t i);
  *               edges_scanned}. edges_scanned (sum of deg over expansions) is
  * an extra counter for the algorithmic-bytes model; it does not alter the
  * algorithm. */
+/* 0: reference-order sq_dist (vecstore.cpp:77-95, default); 1: the B200
+ * library's warp-tree order (its exact_dist = 0 mode), for checking that mode
+ * bit for bit. Applies to the search and the construction search. */
+void pago_set_distance_mode(pago_index* ix, int mode);
 int pago_search(const pago_index* ix, const float* q, uint64_t nq, uint32_t K, uint32_t efS,
                 uint32_t b_override, int use_prt, int use_tfb, uint32_t* ids, float* sq,
                 uint32_t* n_out, uint64_t* stats);

@@ -496,3 +496,25 @@ def test_construction_submit_wait_matches_blocking(pag, built):
         for x, y in ((got.ids, w.ids), (got.sq, w.sq), (got.n_out, w.n_out), (got.stats, w.stats),
                      (got.pes_n, w.pes_n), (got.pes, w.pes)):
             assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("name", ["euc48", "cos20", "tail10", "deg64", "pad9c", "unit256", "unit512", "unit768",
+                                  "unit1024"])
+def test_warp_tree_mode_bitexact_vs_oracle_same_order(pag, built, name):
+    """exact_dist = 0 (warp-tree FMA partials + xor butterfly) is bit-identical
+    to the oracle restating that summation order (pag_oracle.c
+    warp_tree_sq_dist): the traversal is shared, so the mode's differences
+    from the reference come from the summation order alone."""
+    fx = built(name)
+    ix = gpu_index(pag, fx["index"])
+    oix = O.OracleIndex(fx["index"])
+    for K, efS in ((10, 40), (10, 300), (100, 150)):
+        got = ix.search_batch(fx["queries"], pag.SearchParams(K=K, efS=efS, exact_dist=False))
+        want = oix.search(fx["queries"], K, efS, warp_tree=True)
+        assert_same_results((got.ids, got.sq, got.n_out, got.stats), want, f"{name} warp-tree {K}/{efS}")
+    nodes = np.arange(0, oix.n, 11, dtype=np.uint32)
+    got = ix.construction_search(nodes, pag.SearchParams(K=ix.efC, efS=ix.efC, b_override=ix.b_build,
+                                                         exact_dist=False))
+    want = oix.construction_search(nodes, warp_tree=True)
+    assert_same_results((got.ids, got.sq, got.n_out, got.stats), want[:4], f"{name} warp-tree construction")
+    assert np.array_equal(got.pes_n, want[5])

@@ -287,3 +287,20 @@ def test_construction_search_matches_reference(built, fixture_dir, name, kw):
         assert pes_n.sum() > 0  # the fixture exercises the PES path
     else:
         assert pes_n.sum() == 0
+
+
+def test_warp_tree_order_is_a_close_restatement(built):
+    """The oracle's warp-tree summation order (the GPU's exact_dist = 0 mode)
+    stays within 1e-6 relative of the reference order and changes results
+    only at near-ties: on the fixtures the two orders give the same id sets
+    for nearly all queries."""
+    for name in ("euc48", "pad30", "unit768"):
+        fx = built(name)
+        ix = O.OracleIndex(fx["index"])
+        a = ix.search(fx["queries"], 10, 80)
+        b = ix.search(fx["queries"], 10, 80, warp_tree=True)
+        both = a[0] == b[0]
+        rel = np.abs(a[1] - b[1]) / np.maximum(np.abs(a[1]), 1e-30)
+        assert rel[both].max() <= 1e-6
+        same = np.mean([set(a[0][i, :a[2][i]]) == set(b[0][i, :b[2][i]]) for i in range(len(a[2]))])
+        assert same >= 0.98
