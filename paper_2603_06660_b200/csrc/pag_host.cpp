@@ -632,10 +632,12 @@ struct Plan {
 struct Knobs {
     int wpb = 4;
     int hash_log2 = -1, hash_fill = -1;
+    int max_bps = 0;  // cap on resident blocks per SM (0: the occupancy limit)
     long long smem_budget = -1;
     bool debug = false;
     Knobs() {
         if (const char* e = std::getenv("PAG_GPU_WPB")) wpb = std::max(1, std::min(4, std::atoi(e)));
+        if (const char* e = std::getenv("PAG_GPU_MAX_BPS")) max_bps = std::max(0, std::atoi(e));
         if (const char* e = std::getenv("PAG_GPU_HASH_LOG2")) hash_log2 = std::atoi(e);
         if (const char* e = std::getenv("PAG_GPU_HASH_FILL")) hash_fill = std::max(1, std::min(90, std::atoi(e)));
         if (const char* e = std::getenv("PAG_GPU_SMEM_BUDGET")) smem_budget = std::atoll(e);
@@ -745,6 +747,7 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     int bps = 0;
     cuda_check(pagdev::search_occupancy(L, &bps), "occupancy");
     if (bps <= 0) throw_err(PAG_GPU_ERUNTIME, "search configuration does not fit on the GPU");
+    if (kn.max_bps > 0) bps = std::min(bps, kn.max_bps);  // concurrency experiments
     const int want_blocks = static_cast<int>((nq + kWarpsPerBlock - 1) / kWarpsPerBlock);
     pl.grid = std::max(1, std::min(r.num_sms * bps, want_blocks));
     if (kn.debug)

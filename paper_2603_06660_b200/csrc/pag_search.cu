@@ -1557,6 +1557,9 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
                     }
                 }
                 const uint32_t pm = __ballot_sync(FULL, pl);
+                // the radius only shrinks and the test is monotone in it: a
+                // survivor failing now fails at its own (later) turn too
+                rem &= pm;
                 const uint32_t am = __ballot_sync(FULL, pl && sqv < asq);
                 const uint32_t fp = pm & (am ? (am & (0u - am)) - 1u : 0xffffffffu);
                 if (fp) s.push_fp_many(fp, w, sqv, dgv, lane);
