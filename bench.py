@@ -157,6 +157,38 @@ def algorithmic_bytes(stats: np.ndarray, dpad: int, L: int, K: int) -> float:
     return float(bq.sum())
 
 
+def source_sha() -> str:
+    """sha256 of the library's sources (csrc/*.cu|*.cpp|*.h, the Makefile and
+    include/pag_gpu.h): a recorded ncu traffic figure applies only to the
+    kernel built from exactly these sources (the .so itself is rebuilt at
+    round end)."""
+    h = hashlib.sha256()
+    csrc = os.path.join(ROOT, "paper_2603_06660_b200", "csrc")
+    files = sorted(f for f in os.listdir(csrc) if f.endswith((".cu", ".cpp", ".h")) or f == "Makefile")
+    for f in files:
+        h.update(f.encode())
+        h.update(open(os.path.join(csrc, f), "rb").read())
+    h.update(open(os.path.join(ROOT, "include", "pag_gpu.h"), "rb").read())
+    return h.hexdigest()[:16]
+
+
+def recorded_traffic(cfg_name: str, dist: str, efs: int, nq: int):
+    """DRAM bytes per launch of the search kernel from an ncu capture of this
+    exact source tree, workload, distance mode and efS (profiles/ncu_traffic.json,
+    written by tools/ncu_traffic.py), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            recs = json.load(f).get("captures", [])
+    except (OSError, ValueError):
+        return None, None
+    sha = source_sha()
+    for rec in recs:
+        if (rec.get("config") == cfg_name and rec.get("dist") == dist and rec.get("efS") == efs
+                and rec.get("queries_per_launch") == nq and rec.get("source_sha") == sha):
+            return rec["bytes_per_launch"], rec.get("capture")
+    return None, None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -717,15 +749,9 @@ def run_pag(args, cfg, paths, rank, world, local_rank, threads, dist):
         if dist is not None:
             dist.destroy_process_group()
         return
-    # ncu DRAM traffic per launch recorded for this workload/mode/efS (profiles/)
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            rec = json.load(f).get(args.config)
-        if rec and rec["dist"] == args.dist and rec["efS"] == efs and rec["queries_per_launch"] == nq:
-            traffic = rec["bytes_per_launch"]
-    except (OSError, ValueError, KeyError):
-        traffic = None
+    # ncu DRAM traffic per launch recorded for this source tree / workload /
+    # mode / efS (profiles/ncu_traffic.json), else null
+    traffic, traffic_src = recorded_traffic(args.config, args.dist, efs, nq)
     # cpu baseline: the reference search on this host's cores (plain build =
     # the reference's own flags, and the -march=native timing build), all
     # threads over the sample and 1 thread over its first queries
@@ -807,7 +833,8 @@ def run_pag(args, cfg, paths, rank, world, local_rank, threads, dist):
                 "sync_path": "pag_gpu_search, one blocking call per step"},
         "gpu_launches": args.steps,  # one pag_search_kernel launch per step
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
+                     "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_capture": traffic_src,
+                     "source_sha": source_sha(), "peak_kind": peak_kind,
                      "bytes_per_query": round(bytes_total / nq, 1),
                      "algorithmic_bytes_per_launch": round(bytes_total, 1)},
         "per_query": {"exact": round(float(sm[:, 0].mean()), 2), "tests": round(float(sm[:, 1].mean()), 2),
