@@ -11,6 +11,12 @@ namespace pagdev {
 // Per-query status bits written next to the counters.
 enum : uint32_t {
     kStatusZeroCosineQuery = 1u << 0,  // routing.cpp:257 "zero query under cosine metric"
+    // PAG_VALIDATE debug builds only: the device counterpart of
+    // TfbState::validate (routing.cpp:116-137) found a violated invariant
+    kStatusTfbCapacity = 1u << 4,      // "TFB: working set over capacity" / ring size over b
+    kStatusTfbZmax = 1u << 5,          // "TFB: stale z_max"
+    kStatusTfbDuplicate = 1u << 6,     // "TFB: duplicate node residence"
+    kStatusTfbOrder = 1u << 7,         // "TFB: result list out of order"
 };
 
 // Per-query counters (routing.hpp:24-34 plus edges_scanned and status).
@@ -102,6 +108,7 @@ struct SearchLaunch {
     uint32_t off_rf, off_rt, rings_in_smem;
     uint32_t off_rl, rl_in_smem, rl_cap;  // R_L append buffer (+ sort scratch)
     uint32_t off_merge, merge_in_smem;
+    uint32_t off_dbg;  // PAG_VALIDATE builds: per-slot HBM scratch for the resident-id check
     uint32_t warps_per_block;
 };
 

@@ -739,6 +739,12 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     L.off_rt = L.off_rf + 12 * b;
     place(rl_s, szRL, &L.off_rl, &L.rl_in_smem);
     place(m_s, szM, &L.off_merge, &L.merge_in_smem);
+#ifdef PAG_VALIDATE
+    {  // resident ids of W, both rings and R_L (debug check, HBM)
+        uint32_t dbg_flag = 0;
+        place(false, align16(4 * (capr + 3 * b)), &L.off_dbg, &dbg_flag);
+    }
+#endif
     L.warp_smem_bytes = (off + 63u) & ~63u;  // keeps every warp's table 64-B aligned
     pl.gscratch_stride = std::max<uint64_t>(256, goff);
     L.gscratch_stride = pl.gscratch_stride;
@@ -1525,6 +1531,11 @@ void submit_all(pag_gpu_index& ix, uint64_t t, LaunchShard&& launch) {
 
 void check_status(uint32_t so) {
     if (so & pagdev::kStatusZeroCosineQuery) throw_err(PAG_GPU_EINVAL, "zero query under cosine metric");
+    // PAG_VALIDATE builds (routing.cpp:116-137 texts, std::logic_error)
+    if (so & pagdev::kStatusTfbCapacity) throw_err(PAG_GPU_ELOGIC, "TFB: working set over capacity");
+    if (so & pagdev::kStatusTfbZmax) throw_err(PAG_GPU_ELOGIC, "TFB: stale z_max");
+    if (so & pagdev::kStatusTfbDuplicate) throw_err(PAG_GPU_ELOGIC, "TFB: duplicate node residence");
+    if (so & pagdev::kStatusTfbOrder) throw_err(PAG_GPU_ELOGIC, "TFB: result list out of order");
 }
 
 // ix.dup_nodes from the first replica's adjacency (after load / refresh)
@@ -1721,6 +1732,9 @@ int pag_gpu_construction_search(pag_gpu_index* ix, const uint32_t* nodes, uint64
             search_on_replica(*ix, ix->reps[d], p, nullptr, q1 - q0, ids + q0 * p.K, sq + q0 * p.K, n_out + q0,
                               stats ? stats + q0 : nullptr, &status[d], &ch);
         });
+        uint32_t so = 0;
+        for (auto s : status) so |= s;
+        check_status(so);
     });
 }
 

@@ -159,6 +159,9 @@ struct Common {
     __device__ Arr mo() const { return make_arr(mo_base, mo_cap); }
     // counters (routing.hpp:24-34 + edges_scanned)
     uint32_t n_exact, n_test, n_pass, n_visited, n_edges, n_pes;
+#ifdef PAG_VALIDATE
+    uint32_t invalid;  // kStatusTfb* bits found by validate_state
+#endif
 #ifdef PAG_PHASE_TIMING
     long long pt_t0, pt_acc[8];
 #endif
@@ -592,6 +595,24 @@ struct TfbReg {
         c.rl_size += wsize;
         __syncwarp();
     }
+#ifdef PAG_VALIDATE
+    // debug: max sq of W, and the resident ids of W, R_F, R_T -> dst
+    __device__ float w_max(int lane) const {
+        const uint32_t k = static_cast<uint32_t>(lane) < wsize ? fkey(w_sq) : 0u;
+        return __uint_as_float(__reduce_max_sync(FULL, k));
+    }
+    __device__ uint32_t dump_ids(uint32_t* dst, int lane) const {
+        const uint32_t L = static_cast<uint32_t>(lane);
+        if (L < wsize) dst[L] = w_id;
+        for (uint32_t i = L; i < rf_size; i += 32) {
+            uint32_t p = rf_head + i;
+            if (p >= b) p -= b;
+            dst[wsize + i] = rf().id[p];
+        }
+        if (L < b && ((L + b - rt_head) % b) < rt_size) dst[wsize + rf_size + (L + b - rt_head) % b] = t_id;
+        return wsize + rf_size + rt_size;
+    }
+#endif
     // routing.cpp:92-114
     __device__ bool end_round(Common& c, int lane) {
         flush(c, lane);
@@ -979,6 +1000,19 @@ struct TfbMemT {
         rescan(z / S, lane);
         zmax_from_caches();
     }
+#ifdef PAG_VALIDATE
+    __device__ float w_max(int lane) const {
+        uint32_t k = 0;
+        for (uint32_t i = lane; i < wsize; i += 32) k = max(k, fkey(W.sq[i]));
+        return __uint_as_float(__reduce_max_sync(FULL, k));
+    }
+    __device__ uint32_t dump_ids(uint32_t* dst, int lane) const {
+        for (uint32_t i = lane; i < wsize; i += 32) dst[i] = W.id[i];
+        for (uint32_t i = lane; i < rf_size; i += 32) dst[wsize + i] = rf.id[(rf_head + i) % b];
+        for (uint32_t i = lane; i < rt_size; i += 32) dst[wsize + rf_size + i] = rt.id[(rt_head + i) % b];
+        return wsize + rf_size + rt_size;
+    }
+#endif
     __device__ void flush(Common& c, int lane) {
         for (uint32_t i = lane; i < wsize; i += 32) rl_append(c, W.id[i], W.sq[i], true, i);
         c.rl_size += wsize;
@@ -1627,6 +1661,40 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
     return track_pes && !pes_ok;
 }
 
+#ifdef PAG_VALIDATE
+// Debug builds: the device counterpart of TfbState::validate
+// (routing.cpp:116-137), run after every expansion and end_round. Checks
+// capacities (W, both rings <= b), that z_max is the largest sq in W, and
+// that no node resides twice across W, R_F, R_T and the flushed R_L entries
+// (the reference's bounded sorted R_L is formed here only at the end; its
+// order is checked there). Violations set kStatusTfb* bits in the query's
+// status; the host raises the reference's logic_error texts.
+template <class TFB>
+__device__ void validate_state(const SearchLaunch& P, Common& c, TFB& s, uint8_t* gw, int lane) {
+    uint32_t bad = 0;
+    if (s.wsize > P.b || s.rf_size > P.b || s.rt_size > P.b) bad |= kStatusTfbCapacity;
+    const float mx = s.w_max(lane);
+    if (s.wsize && fkey(mx) != fkey(s.zmax_sq)) bad |= kStatusTfbZmax;
+    uint32_t* dbg = reinterpret_cast<uint32_t*>(gw + P.off_dbg);
+    uint32_t n = s.dump_ids(dbg, lane);
+    const Arr rl = c.rl();
+    for (uint32_t i = lane; i < c.rl_size; i += 32) dbg[n + i] = rl.id[i];
+    n += c.rl_size;
+    __syncwarp();
+    bool dup = false;
+    for (uint32_t i = 0; i < n; ++i) {
+        const uint32_t x = dbg[i];
+        for (uint32_t j = i + 1 + lane; j < n; j += 32) dup |= dbg[j] == x;
+    }
+    if (__any_sync(FULL, dup)) bad |= kStatusTfbDuplicate;
+    __syncwarp();
+    c.invalid |= bad;
+}
+#define PAG_VALIDATE_STATE() validate_state(P, c, s, gw, lane)
+#else
+#define PAG_VALIDATE_STATE() do { } while (0)
+#endif
+
 template <class TFB, bool EXACT, int NCH, bool PES>
 #ifndef PAG_MIN_BLOCKS
 #define PAG_MIN_BLOCKS PAG_OCC
@@ -1696,6 +1764,9 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
         c.gt_count = 0;
         c.gt_used = false;
         c.n_exact = c.n_test = c.n_pass = c.n_visited = c.n_edges = c.n_pes = 0;
+#ifdef PAG_VALIDATE
+        c.invalid = 0;
+#endif
         s.reset();
         for (uint32_t i = lane; i < (1u << c.hs_log2) / 4; i += 32)
             reinterpret_cast<uint4*>(c.hs)[i] = make_uint4(EMPTY, EMPTY, EMPTY, EMPTY);
@@ -1835,6 +1906,7 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
         }
 
         PT(0);
+        PAG_VALIDATE_STATE();
         // ---- rounds (routing.cpp:229-240)
         for (uint32_t r = 0; r < P.r_max; ++r) {
             while (true) {
@@ -1847,9 +1919,11 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
                         P.out_pes[static_cast<uint64_t>(qid) * P.pes_cap + c.n_pes] = u;
                     ++c.n_pes;
                 }
+                PAG_VALIDATE_STATE();
             }
             PT(2);
             if (r + 1 == P.r_max || !s.end_round(c, lane)) break;
+            PAG_VALIDATE_STATE();
             PT(7);
         }
         // final flush (routing.cpp:242) and truncation to K (:244-246)
@@ -1861,6 +1935,14 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
         for (uint32_t i = lane; i < c.rl_size; i += 32) c.rl().aux[i] = 0u;
         __syncwarp();
         const Arr res = warp_sort(c.rl(), c.rl_tmp(), c.rl_size, lane);
+#ifdef PAG_VALIDATE
+        {  // routing.cpp:132-134: result list order (the sorted list R_L is cut from)
+            bool bad_order = false;
+            for (uint32_t i = lane + 1; i < c.rl_size; i += 32)
+                bad_order |= cless(res.sq[i], res.id[i], res.sq[i - 1], res.id[i - 1]);
+            if (__any_sync(FULL, bad_order)) c.invalid |= kStatusTfbOrder;
+        }
+#endif
         release();
         for (uint32_t i = lane; i < k_out; i += 32) {
             P.out_ids[static_cast<uint64_t>(qid) * P.K + i] = res.id[i];
@@ -1875,7 +1957,11 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
             st[kStatPass] = c.n_pass;
             st[kStatVisited] = c.n_visited;
             st[kStatEdges] = c.n_edges;
+#ifdef PAG_VALIDATE
+            st[kStatStatus] = c.invalid;
+#else
             st[kStatStatus] = 0u;
+#endif
             st[6] = c.hs_count + c.gt_count;  // marks held
             st[7] = c.gt_count;               // of which in the HBM bitmap
             if (P.out_pes_n) P.out_pes_n[qid] = c.n_pes;
