@@ -1071,7 +1071,10 @@ def run_construction(args, cfg, paths, rank, world, local_rank, threads, dist):
                         "preallocated result sets"},
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind,
+                     "frac": round(achieved / peak, 4),
+                     "traffic": recorded_traffic(f"{args.config}-construction", "exact", K, nn)[0],
+                     "traffic_capture": recorded_traffic(f"{args.config}-construction", "exact", K, nn)[1],
+                     "source_sha": source_sha(), "peak_kind": peak_kind,
                      "bytes_per_query": round(bytes_total / nn, 1),
                      "algorithmic_bytes_per_launch": round(bytes_total, 1)},
         "per_node": {"exact": round(float(sm[:, 0].mean()), 2), "tests": round(float(sm[:, 1].mean()), 2),
