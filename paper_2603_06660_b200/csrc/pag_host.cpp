@@ -1046,8 +1046,7 @@ uint64_t ground_truth_on_replica(pag_gpu_index& ix, Replica& r, const float* q, 
         //    any k distinct rows give the bound)
         pag_search_params sp;
         pag_gpu_default_params(&sp);
-        sp.K = kk;
-        sp.efS = 2 * kk;  // two rounds: k rows for nearly every query (efS = k left cfg-2 k = 100 24 short)
+        sp.K = sp.efS = kk;
         sp.exact_dist = 0;
         DevBuf rawq(4ull * nq * ix.dim), sids(4ull * nq * kk), ssq(4ull * nq * kk), sn(4ull * nq),
             sst(4ull * nq * pagdev::kStatWords);
