@@ -1043,10 +1043,7 @@ uint64_t ground_truth_on_replica(pag_gpu_index& ix, Replica& r, const float* q, 
     std::vector<uint32_t> redo;
     if (pool) {
         // 1. k rows per query from a graph search of the raw query (ids only;
-        //    any k distinct rows give the bound). A query whose search returns
-        //    fewer than k rows (its PRT-filtered region held fewer) gets no
-        //    bound and joins the exact re-run, which costs about one base pass
-        //    per 64 such queries
+        //    any k distinct rows give the bound)
         pag_search_params sp;
         pag_gpu_default_params(&sp);
         sp.K = sp.efS = kk;
