@@ -111,7 +111,9 @@ int pag_gpu_search(pag_gpu_index* ix, const float* q, uint64_t nq,
  * synchronisation. For resident-input throughput measurement and for
  * callers that keep queries on the GPU. Consecutive launches on one stream
  * overlap (programmatic dependent launch); a launch on a different stream
- * than the handle's previous one first waits for that stream's work. */
+ * than the handle's previous one first waits for that stream's work (an
+ * event recorded there at the switch), so a caller stream must stay valid
+ * until the handle's next launch on another stream or its close. */
 int pag_gpu_search_device(pag_gpu_index* ix, const float* q_dev, uint64_t nq,
                           const pag_search_params* params, uint32_t* ids_dev, float* sq_dev,
                           uint32_t* n_out_dev, uint32_t* stats_dev, void* stream);
