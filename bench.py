@@ -157,18 +157,30 @@ def algorithmic_bytes(stats: np.ndarray, dpad: int, L: int, K: int) -> float:
     return float(bq.sum())
 
 
+def _code_only(text: str, makefile: bool = False) -> str:
+    """Source text without comments and blank lines (comment edits do not
+    change the built kernel)."""
+    import re
+    if makefile:
+        text = re.sub(r"(?m)^\s*#.*$", "", text)
+    else:
+        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+        text = re.sub(r"(?m)//.*$", "", text)
+    return "\n".join(line.rstrip() for line in text.splitlines() if line.strip())
+
+
 def source_sha() -> str:
-    """sha256 of the library's sources (csrc/*.cu|*.cpp|*.h, the Makefile and
-    include/pag_gpu.h): a recorded ncu traffic figure applies only to the
-    kernel built from exactly these sources (the .so itself is rebuilt at
-    round end)."""
+    """sha256 of the library's sources without comments (csrc/*.cu|*.cpp|*.h,
+    the Makefile and include/pag_gpu.h): a recorded ncu traffic figure applies
+    only to the kernel built from exactly this code (the .so itself is rebuilt
+    at round end and its bytes are not reproducible)."""
     h = hashlib.sha256()
     csrc = os.path.join(ROOT, "paper_2603_06660_b200", "csrc")
     files = sorted(f for f in os.listdir(csrc) if f.endswith((".cu", ".cpp", ".h")) or f == "Makefile")
     for f in files:
         h.update(f.encode())
-        h.update(open(os.path.join(csrc, f), "rb").read())
-    h.update(open(os.path.join(ROOT, "include", "pag_gpu.h"), "rb").read())
+        h.update(_code_only(open(os.path.join(csrc, f)).read(), f == "Makefile").encode())
+    h.update(_code_only(open(os.path.join(ROOT, "include", "pag_gpu.h")).read()).encode())
     return h.hexdigest()[:16]
 
 
