@@ -108,3 +108,11 @@ def test_reference_arm_imports_no_native_library():
             % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
     assert out.returncode == 0 and out.stdout.strip() == "ok", out.stderr
+
+
+def test_source_hash_ignores_comments():
+    a = "int f() { /* a\n b */ return 1; // c\n}\n"
+    b = "int f() {\n  return 1;\n}\n"
+    assert bench._code_only(a).replace(" ", "") == bench._code_only(b).replace(" ", "")
+    assert bench._code_only("X := 1\n# note\n", makefile=True) == "X := 1"
+    assert len(bench.source_sha()) == 16
