@@ -1426,7 +1426,7 @@ void free_slot(pag_gpu_index& ix, Replica& r, uint64_t ticket) {
     const uint64_t old = a.ticket;
     uint32_t so = 0;
     async_complete(r, a, &so);
-    ix.early_status[old] |= so;
+    if (so) ix.early_status[old] |= so;  // only failures need keeping (a later wait of an OK ticket returns OK)
 }
 
 void async_submit_replica(pag_gpu_index& ix, Replica& r, const pag_search_params& p, const float* q,
