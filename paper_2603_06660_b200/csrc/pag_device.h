@@ -38,14 +38,19 @@ enum : uint32_t {
 //           base_offset f32[S] | codes u32[S][cwp]   (edge-major codes)
 //  refsT  : L x sub_dim x m fp32 (reference family, transposed so one
 //           subspace's m references are contiguous per component)
+//  rowsX  : n x xstride fp32, the chain-interleaved copy of rows read by the
+//           reference-order distances (built on the device at the first
+//           search that needs it, see chain_positions / launch_interleave_rows)
 struct IndexView {
     const float* rows;
+    const float* rowsX;
     const uint32_t* deg;
     const uint8_t* adj;
     const float* refsT;
     const uint32_t* entries;
     uint64_t n;
     uint32_t dim, padded, dstride;
+    uint32_t xstride;  // floats per rowsX row (multiple of 32)
     uint32_t L, m, sub_dim;
     uint32_t slot_stride, cwp, block_bytes;
     uint32_t n_entries;
@@ -103,7 +108,6 @@ struct SearchLaunch {
     uint32_t warp_smem_bytes;
     uint32_t off_q, off_T, off_hash, hash_log2, off_sqbuf;
     uint32_t hash_limit;  // marks the smem table takes before spilling to the bitmap
-    uint32_t off_stage;
     uint32_t off_W, W_in_smem;
     uint32_t off_rf, off_rt, rings_in_smem;
     uint32_t off_rl, rl_in_smem, rl_cap;  // R_L append buffer (+ sort scratch)
@@ -188,6 +192,23 @@ struct GtTcPoolLaunch {
     uint32_t* uncertified;      // nq flags: 1 = re-run exactly
 };
 cudaError_t launch_gt_tc_pool(const GtTcPoolLaunch& g, cudaStream_t stream);
+
+// Chain-interleaved row layout (reference-order distances, vecstore.cpp:77-95).
+// sq_dist runs four accumulator chains: chain c takes elements c, c + 4, ...
+// of the first D4 = padded & ~3 elements, and chain 0 then takes the tail
+// elements D4 .. padded-1. Call "position" p the p-th step of the chains:
+// p < D4/4 holds elements 4p .. 4p+3 (one per chain), position D4/4 + t holds
+// tail element D4 + t for chain 0 and zeros for chains 1-3 (a zero difference
+// adds +0 to a chain: no change). Positions are padded with zeros to a
+// multiple of 8, and every 8 positions are stored as one 128-B line
+//   chain 0: 8 floats | chain 1: 8 floats | chain 2: 8 floats | chain 3: 8 floats
+// so that the lane running chain c of a row reads its next 8 elements with
+// one 32-B load, and the 4 lanes of a row read whole lines.
+__host__ __device__ inline uint32_t chain_positions(uint32_t padded) { return (padded >> 2) + (padded & 3u); }
+__host__ __device__ inline uint32_t chain_xstride(uint32_t padded) { return ((chain_positions(padded) + 7u) >> 3) << 5; }
+// rows (n x dstride) -> rowsX (n x chain_xstride(padded)), rows [first, n)
+cudaError_t launch_interleave_rows(const float* rows, float* rowsX, uint64_t first, uint64_t n, uint32_t padded,
+                                   uint32_t dstride, cudaStream_t stream);
 
 // pag_util.cu: staged node blocks -> their slots in the adjacency array
 cudaError_t scatter_blocks(const void* staging, const uint32_t* ids, uint32_t count, void* adj,

@@ -168,6 +168,11 @@ struct Replica {
     float* refsT = nullptr;
     uint32_t* entries = nullptr;
     float* bnorm = nullptr;  // squared row norms (from the file's cached norms), GT only
+    // chain-interleaved copy of the rows (pag_device.h chain_positions), read
+    // by the reference-order distances; built at the first such search and
+    // extended after a refresh (rows are only ever appended)
+    float* rows_x = nullptr;
+    uint64_t rows_x_n = 0, rows_x_cap = 0;  // rows interleaved so far / allocated
     uint64_t cap_nodes = 0;  // allocated node capacity (refresh grows it)
     size_t bytes = 0;
     // search scratch
@@ -322,6 +327,8 @@ struct pag_gpu_index {
     pagdev::IndexView view(const Replica& r) const {
         pagdev::IndexView v{};
         v.rows = r.rows;
+        v.rowsX = r.rows_x;
+        v.xstride = pagdev::chain_xstride(padded);
         v.deg = r.deg;
         v.adj = r.adj;
         v.refsT = r.refsT;
@@ -355,7 +362,8 @@ void free_replica(Replica& r) {
                     static_cast<void*>(r.refsT), static_cast<void*>(r.entries),
                     static_cast<void*>(r.gbm),
                     static_cast<void*>(r.gscratch), static_cast<void*>(r.qcounter),
-                    static_cast<void*>(r.d_q), static_cast<void*>(r.d_out), static_cast<void*>(r.bnorm)})
+                    static_cast<void*>(r.d_q), static_cast<void*>(r.d_out), static_cast<void*>(r.bnorm),
+                    static_cast<void*>(r.rows_x)})
         dev_free(p);
     if (r.h_pin) cudaFreeHost(r.h_pin);
     for (auto& a : r.aslot) {
@@ -692,7 +700,8 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     // fixed smem regions
     uint32_t off = 0;
     L.off_q = off;
-    off = align16(off + 4 * ix.dstride);
+    // (reference-order mode: the query is re-laid chain-interleaved in place)
+    off = align16(off + 4 * (p.exact_dist ? std::max(ix.dstride, pagdev::chain_xstride(ix.padded)) : ix.dstride));
     off = (off + 63u) & ~63u;  // 64-B aligned table (code_sum ORs the code offset into the base)
     L.off_T = off;
     off = align16(off + 4 * ix.L * 16);  // T rows padded to 16 (m <= 16)
@@ -700,8 +709,6 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     off = align16(off + (4u << L.hash_log2));
     L.off_sqbuf = off;
     off = align16(off + 256);
-    L.off_stage = off;
-    if (p.exact_dist) off = align16(off + 4 * 36 * 16);  // transposed chain staging (exact mode only)
     // movable regions: W (12b), rings (24b), R_L (24 capr), merge (48b);
     // with b <= 32 the working set and R_T live in registers
     // (b <= 32: the rings region holds R_F only, 32 slots; R_T is in registers)
@@ -786,6 +793,26 @@ void ensure_scratch(Replica& r, Plan& pl) {
     L.qbase = r.qbase[par];
 }
 
+// the chain-interleaved row copy of a replica, complete for the current n
+// (first reference-order search, or the first one after a refresh); blocking,
+// so that any stream may launch afterwards
+void ensure_rows_x(pag_gpu_index& ix, Replica& r) {
+    if (r.rows_x && r.rows_x_n == ix.n) return;
+    const size_t xrow = 4ull * pagdev::chain_xstride(ix.padded);
+    if (r.rows_x_cap < ix.n) {
+        dev_free(r.rows_x);  // (cudaFree waits for running kernels)
+        r.rows_x = nullptr;
+        r.rows_x_n = r.rows_x_cap = 0;
+        const uint64_t cap = std::max<uint64_t>(ix.n, r.cap_nodes);
+        dev_alloc(&r.rows_x, cap * xrow);
+        r.rows_x_cap = cap;
+    }
+    cuda_check(pagdev::launch_interleave_rows(r.rows, r.rows_x, r.rows_x_n, ix.n, ix.padded, ix.dstride, r.stream),
+               "interleave rows");
+    cuda_check(cudaStreamSynchronize(r.stream), "interleave rows");
+    r.rows_x_n = ix.n;
+}
+
 void validate_params(const pag_gpu_index& ix, const pag_search_params& p) {
     if (ix.n == 0) throw_err(PAG_GPU_ERUNTIME, "search on empty index");  // routing.cpp:208
     if (p.K > p.efS) throw_err(PAG_GPU_EINVAL, "K > efS");                // routing.cpp:209
@@ -812,6 +839,7 @@ void run_search(pag_gpu_index& ix, Replica& r, const pag_search_params& p, const
                 uint32_t nq, uint32_t* ids, float* sq, uint32_t* n_out, uint32_t* stats, cudaStream_t stream,
                 const ConstructionArgs* ca = nullptr, const AsyncArgs* aa = nullptr) {
     if (nq == 0) return;
+    if (p.exact_dist) ensure_rows_x(ix, r);
     Plan pl = make_plan(ix, r, p, nq);
     ensure_scratch(r, pl);
     // one launch order per replica: a launch on another stream than the last

@@ -65,7 +65,6 @@ __device__ unsigned long long g_phase[8];
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint32_t EMPTY = 0xffffffffu;
 constexpr uint32_t VISITED = 0x80000000u;
-constexpr int XSTR = 36;        // floats per transposed chain row in the staging buffer
 
 __device__ __forceinline__ bool cless(float sa, uint32_t ia, float sb, uint32_t ib) {
     return sa < sb || (sa == sb && ia < ib);  // candidate_less, builder.hpp:23-25
@@ -133,7 +132,6 @@ __device__ __forceinline__ Arr make_arr(uint8_t* base, uint32_t cap) {
 struct Common {
     float* q;
     float* T;
-    float* stage;
     float* sqbuf;
     __device__ uint32_t* degbuf() const { return reinterpret_cast<uint32_t*>(sqbuf + 32); }
     // visited marks (routing.hpp:104-105): smem open addressing; once the
@@ -1069,17 +1067,15 @@ struct TfbMemT {
 // ---------------------------------------------------------------------------
 // Exact squared distances for the rows named by lanes in `items` (lane j:
 // row id w). Results land in c.sqbuf[j], deg[w] in c.degbuf()[j].
-// EXACT: the reference order (vecstore.cpp:77-95). All 32 lanes compute the
-//   squared differences of a 128-float chunk (coalesced float4 loads, one
-//   chunk of look-ahead, packed f32x2 arithmetic) and scatter them transposed
-//   into smem; 4 lanes per row then run the four strided accumulator chains
-//   serially (8 x LDS.128 + 32 FADD per chunk).
+// EXACT: the reference order (vecstore.cpp:77-95), from the chain-interleaved
+//   row copy: 4 lanes per row run the four strided accumulator chains
+//   serially, 8 rows per batch (dist_exact_x).
 // !EXACT: lane-parallel packed-FMA partials + xor tree (within 1e-5 rel).
 // NCH > 0: padded_dim == dstride == 128 * NCH (compile-time chunk count);
-// NCH == 0: any padded_dim (bounds checks, reference tail handling).
+// NCH == 0: any padded_dim.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ float2 sq2(float2 v, float2 q) {  // (v - q)^2 per component, no contraction
-    const float2 d = __fadd2_rn(v, make_float2(-q.x, -q.y));
+__device__ __forceinline__ float2 sq2n(float2 v, float2 nq) {  // (v + nq)^2 per component, no contraction
+    const float2 d = __fadd2_rn(v, nq);
     return __fmul2_rn(d, d);
 }
 
@@ -1097,163 +1093,112 @@ __device__ __forceinline__ int take_batch(uint32_t& rest, int (&jr)[4]) {
     return nb;
 }
 
-template <int NCH>
-__device__ void dist_exact(const SearchLaunch& P, Common& c, uint32_t items, uint32_t w, int lane) {
+// Reference-order distances (vecstore.cpp:77-95) from the chain-interleaved
+// row copy (pag_device.h chain_positions): lane 4r + c runs accumulator chain
+// c of the batch's r-th row, up to 8 rows per batch. A 128-B line of rowsX
+// holds 8 consecutive elements of each of the four chains, so the lane's
+// next 8 chain elements are one 32-B load (the four lanes of a row read whole
+// lines) and no transposition is needed: packed differences and squares, then
+// the 8 serial adds of the chain. The tail elements of a padded_dim that is
+// not a multiple of 4 are extra chain-0 positions in the layout (zeros for
+// the other chains), and the layout's zero padding adds +0 to every chain,
+// so any shape runs the same loop. The query is laid out the same way in
+// smem, negated (interleave_query): x - q is computed as x + (-q), the same
+// value bit for bit. NLN: lines per row, 0 = run-time count.
+struct F8 {
+    float4 lo, hi;
+};
+__device__ __forceinline__ F8 ldg_f8(const float* p) {
+    F8 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
+                 : "=f"(v.lo.x), "=f"(v.lo.y), "=f"(v.lo.z), "=f"(v.lo.w), "=f"(v.hi.x), "=f"(v.hi.y),
+                   "=f"(v.hi.z), "=f"(v.hi.w)
+                 : "l"(p), "l"(row_policy()));
+    return v;
+}
+
+template <int NLN>
+__device__ void dist_exact_x(const SearchLaunch& P, Common& c, uint32_t items, uint32_t w, int lane) {
+    constexpr int LA = NLN ? (PAG_OCC >= 6 ? 3 : 6) : 2;  // lines in flight per lane (register budget)
     const IndexView& ix = P.ix;
-    const uint32_t DS = NCH ? 128u * NCH : ix.dstride;
-    const uint32_t D = NCH ? DS : ix.padded, D4 = D & ~3u;
-    const uint32_t nch = NCH ? NCH : (DS + 127u) / 128u;
+    const uint32_t XS = NLN ? 32u * NLN : ix.xstride;
+    const uint32_t nln = NLN ? NLN : XS / 32u;
     const int cr = lane >> 2, cc = lane & 3;
     uint32_t rest = items;
     while (rest) {
-        int jr[4];
-        const int nb = take_batch(rest, jr);
-        const float* rp[4];
+        // this lane's row: the cr-th remaining survivor (none: idle lane)
+        int jm = -1;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            // rows past nb alias row 0 (L1 hits), so loads need no predicate
-            const uint32_t wr = __shfl_sync(FULL, w, r < nb ? jr[r] : jr[0]);
-            rp[r] = ix.rows + static_cast<uint64_t>(wr) * DS + 4u * lane;
+        for (int r = 0; r < 8; ++r) {
+            if (rest) {
+                if (r == cr) jm = __ffs(rest) - 1;
+                rest &= rest - 1;
+            }
         }
+        const uint32_t wr = __shfl_sync(FULL, w, jm < 0 ? 0 : jm);
         float acc = 0.0f;
-        float4 cur[4], nxt[4];
-        const bool in0 = NCH || 4u * lane < DS;
+        if (jm >= 0) {
+            const float* rp = ix.rowsX + static_cast<uint64_t>(wr) * XS + 8u * cc;
+            const float* qp = c.q + 8u * cc;
+            F8 buf[LA];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) cur[r] = in0 ? ldg_f4(rp[r]) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll(NCH ? NCH : 1)
-        for (uint32_t ch = 0; ch < nch; ++ch) {
-            const uint32_t base = 128u * ch;
-            const uint32_t kn = base + 128u + 4u * lane;
-            const bool inn = NCH ? (ch + 1 < nch) : (kn < DS);
+            for (int i = 0; i < LA; ++i)
+                if (NLN ? (i < NLN) : (static_cast<uint32_t>(i) < nln)) buf[i] = ldg_f8(rp + 32 * i);
+#pragma unroll(NLN ? (NLN + LA - 1) / LA : 1)
+            for (uint32_t l0 = 0; l0 < nln; l0 += LA) {
 #pragma unroll
-            for (int r = 0; r < 4; ++r)
-                nxt[r] = inn ? ldg_f4(rp[r] + base + 128u) : make_float4(0.f, 0.f, 0.f, 0.f);
-            const bool in = NCH || base + 4u * lane < DS;
-            const float4 qv = in ? *reinterpret_cast<const float4*>(c.q + base + 4u * lane)
-                                 : make_float4(0.f, 0.f, 0.f, 0.f);
-            float* st = c.stage + lane;
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                if (r < nb) {
-                    const float2 lo = sq2(make_float2(cur[r].x, cur[r].y), make_float2(qv.x, qv.y));
-                    const float2 hi = sq2(make_float2(cur[r].z, cur[r].w), make_float2(qv.z, qv.w));
-                    st[(r * 4 + 0) * XSTR] = lo.x;
-                    st[(r * 4 + 1) * XSTR] = lo.y;
-                    st[(r * 4 + 2) * XSTR] = hi.x;
-                    st[(r * 4 + 3) * XSTR] = hi.y;
-                }
-            }
-            __syncwarp();
-            if (cr < nb) {
-                const float* sp = c.stage + (cr * 4 + cc) * XSTR;
-                if (NCH || base + 128 <= D4) {
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const float4 x = *reinterpret_cast<const float4*>(sp + 4 * i);
-                        acc = __fadd_rn(acc, x.x);
-                        acc = __fadd_rn(acc, x.y);
-                        acc = __fadd_rn(acc, x.z);
-                        acc = __fadd_rn(acc, x.w);
-                    }
-                } else {
-                    const float* s0 = c.stage + (cr * 4) * XSTR;
-                    for (int t = 0; t < 32; ++t) {
-                        const uint32_t kk = base + 4u * t + cc;
-                        if (kk < D4) {
-                            acc = __fadd_rn(acc, sp[t]);
-                        } else if (cc == 0 && kk < D) {
-                            // tail elements all go to acc0, in order (vecstore.cpp:90-93)
-                            acc = __fadd_rn(acc, s0[t]);
-                            if (kk + 1 < D) acc = __fadd_rn(acc, s0[XSTR + t]);
-                            if (kk + 2 < D) acc = __fadd_rn(acc, s0[2 * XSTR + t]);
-                        }
+                for (int i = 0; i < LA; ++i) {
+                    const uint32_t l = l0 + i;
+                    if (l < nln) {
+                        const F8 v = buf[i];
+                        if (l + LA < nln) buf[i] = ldg_f8(rp + 32u * (l + LA));
+                        const float4 q0 = *reinterpret_cast<const float4*>(qp + 32u * l);
+                        const float4 q1 = *reinterpret_cast<const float4*>(qp + 32u * l + 4);
+                        const float2 e0 = sq2n(make_float2(v.lo.x, v.lo.y), make_float2(q0.x, q0.y));
+                        const float2 e1 = sq2n(make_float2(v.lo.z, v.lo.w), make_float2(q0.z, q0.w));
+                        const float2 e2 = sq2n(make_float2(v.hi.x, v.hi.y), make_float2(q1.x, q1.y));
+                        const float2 e3 = sq2n(make_float2(v.hi.z, v.hi.w), make_float2(q1.z, q1.w));
+                        acc = __fadd_rn(acc, e0.x);
+                        acc = __fadd_rn(acc, e0.y);
+                        acc = __fadd_rn(acc, e1.x);
+                        acc = __fadd_rn(acc, e1.y);
+                        acc = __fadd_rn(acc, e2.x);
+                        acc = __fadd_rn(acc, e2.y);
+                        acc = __fadd_rn(acc, e3.x);
+                        acc = __fadd_rn(acc, e3.y);
                     }
                 }
             }
-            __syncwarp();
-#pragma unroll
-            for (int r = 0; r < 4; ++r) cur[r] = nxt[r];
         }
         const float a1 = __shfl_down_sync(FULL, acc, 1);
         const float a2 = __shfl_down_sync(FULL, acc, 2);
         const float a3 = __shfl_down_sync(FULL, acc, 3);
-        int jmine = jr[0];
-#pragma unroll
-        for (int r = 1; r < 4; ++r)
-            if (r == cr) jmine = jr[r];
-        if (cc == 0 && cr < nb) c.sqbuf[jmine] = __fadd_rn(__fadd_rn(acc, a1), __fadd_rn(a2, a3));
+        if (cc == 0 && jm >= 0) c.sqbuf[jm] = __fadd_rn(__fadd_rn(acc, a1), __fadd_rn(a2, a3));
     }
 }
 
-// dist_exact for a compile-time chunk count with two chunks of look-ahead
-// (three rotating register buffers): the next-but-one chunk's loads are in
-// flight while the current chunk's chains run
-template <int NCH>
-__device__ void dist_exact_la2(const SearchLaunch& P, Common& c, uint32_t items, uint32_t w, int lane) {
-    static_assert(NCH >= 2, "two chunks of look-ahead");
-    const IndexView& ix = P.ix;
-    constexpr uint32_t DS = 128u * NCH;
-    const int cr = lane >> 2, cc = lane & 3;
-    uint32_t rest = items;
-    while (rest) {
-        int jr[4];
-        const int nb = take_batch(rest, jr);
-        const float* rp[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const uint32_t wr = __shfl_sync(FULL, w, r < nb ? jr[r] : jr[0]);
-            rp[r] = ix.rows + static_cast<uint64_t>(wr) * DS + 4u * lane;
-        }
-        float acc = 0.0f;
-        float4 buf[3][4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            buf[0][r] = ldg_f4(rp[r]);
-            buf[1][r] = ldg_f4(rp[r] + 128u);
-        }
-#pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) {
-            if (ch + 2 < NCH) {
-#pragma unroll
-                for (int r = 0; r < 4; ++r) buf[(ch + 2) % 3][r] = ldg_f4(rp[r] + 128u * (ch + 2));
-            }
-            const float4 qv = *reinterpret_cast<const float4*>(c.q + 128u * ch + 4u * lane);
-            float* st = c.stage + lane;
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                if (r < nb) {
-                    const float4 v = buf[ch % 3][r];
-                    const float2 lo = sq2(make_float2(v.x, v.y), make_float2(qv.x, qv.y));
-                    const float2 hi = sq2(make_float2(v.z, v.w), make_float2(qv.z, qv.w));
-                    st[(r * 4 + 0) * XSTR] = lo.x;
-                    st[(r * 4 + 1) * XSTR] = lo.y;
-                    st[(r * 4 + 2) * XSTR] = hi.x;
-                    st[(r * 4 + 3) * XSTR] = hi.y;
-                }
-            }
-            __syncwarp();
-            if (cr < nb) {
-                const float* sp = c.stage + (cr * 4 + cc) * XSTR;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const float4 x = *reinterpret_cast<const float4*>(sp + 4 * i);
-                    acc = __fadd_rn(acc, x.x);
-                    acc = __fadd_rn(acc, x.y);
-                    acc = __fadd_rn(acc, x.z);
-                    acc = __fadd_rn(acc, x.w);
-                }
-            }
-            __syncwarp();
-        }
-        const float a1 = __shfl_down_sync(FULL, acc, 1);
-        const float a2 = __shfl_down_sync(FULL, acc, 2);
-        const float a3 = __shfl_down_sync(FULL, acc, 3);
-        int jmine = jr[0];
-#pragma unroll
-        for (int r = 1; r < 4; ++r)
-            if (r == cr) jmine = jr[r];
-        if (cc == 0 && cr < nb) c.sqbuf[jmine] = __fadd_rn(__fadd_rn(acc, a1), __fadd_rn(a2, a3));
+// the padded query in smem, negated and re-laid chain-interleaved in place
+// (after the projection table and the cosine norm have read it as it was):
+// elements below D4 = padded & ~3 move inside their own 32-float block, the
+// <= 3 tail elements become extra chain-0 positions
+__device__ void interleave_query(float* q, uint32_t padded, uint32_t xstride, int lane) {
+    const uint32_t D4 = padded & ~3u, P = D4 >> 2;
+    const bool tail = lane < 3 && D4 + lane < padded;
+    const float tv = tail ? q[D4 + lane] : 0.0f;
+    __syncwarp();
+    const uint32_t dst = 8u * (lane & 3) + (lane >> 2);
+    for (uint32_t b0 = 0; b0 < xstride; b0 += 32) {
+        const uint32_t k = b0 + lane;
+        const float v = k < D4 ? -q[k] : 0.0f;
+        __syncwarp();
+        q[b0 + dst] = v;
     }
+    __syncwarp();
+    if (tail) {
+        const uint32_t p = P + lane;
+        q[((p >> 3) << 5) + (p & 7u)] = -tv;
+    }
+    __syncwarp();
 }
 
 // Warp-tree distances, two rows at a time: each half-warp owns one row and
@@ -1376,18 +1321,15 @@ __device__ __forceinline__ void distances(const SearchLaunch& P, Common& c, uint
     const bool mine = (items >> lane) & 1u;
     uint32_t deg = 0;
     if (mine) {
-        prefetch_row(ix.rows + static_cast<uint64_t>(w) * ix.dstride, ix.dstride * 4u);
+        if (EXACT)
+            prefetch_row(ix.rowsX + static_cast<uint64_t>(w) * ix.xstride, ix.xstride * 4u);
+        else
+            prefetch_row(ix.rows + static_cast<uint64_t>(w) * ix.dstride, ix.dstride * 4u);
         deg = __ldg(ix.deg + w);  // consumed after the rows: its latency overlaps theirs
     }
     if (EXACT) {
-        if constexpr (NCH > 0 && NCH <= 6) {
-            if constexpr (NCH >= 2)
-                dist_exact_la2<(NCH >= 2 ? NCH : 2)>(P, c, items, w, lane);
-            else
-                dist_exact<NCH>(P, c, items, w, lane);
-        } else {
-            dist_exact<NCH>(P, c, items, w, lane);
-        }
+        // padded_dim == 128 NCH: the interleaved row has 4 NCH lines
+        dist_exact_x<4 * NCH>(P, c, items, w, lane);
     } else {
         if constexpr (NCH > 0 && NCH <= 8) {
             dist_fast_pairs<NCH>(P, c, items, w, lane);
@@ -1716,7 +1658,6 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
     c.q = reinterpret_cast<float*>(sw + P.off_q);
     c.T = reinterpret_cast<float*>(sw + P.off_T);
     c.sqbuf = reinterpret_cast<float*>(sw + P.off_sqbuf);
-    c.stage = reinterpret_cast<float*>(sw + P.off_stage);
     {
         uint8_t* rl = (P.rl_in_smem ? sw : gw) + P.off_rl;
         const uint32_t cap = P.rl_cap;  // >= all W flushes of a query (r_max * b + b)
@@ -1824,8 +1765,12 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
                     --room;
                 }
             }
-            if ((seed_sel[0] >> lane) & 1u)
-                prefetch_l2_bulk(ix.rows + static_cast<uint64_t>(seed_id[0]) * ix.dstride, ix.dstride * 4u);
+            if ((seed_sel[0] >> lane) & 1u) {
+                if (EXACT)
+                    prefetch_l2_bulk(ix.rowsX + static_cast<uint64_t>(seed_id[0]) * ix.xstride, ix.xstride * 4u);
+                else
+                    prefetch_l2_bulk(ix.rows + static_cast<uint64_t>(seed_id[0]) * ix.dstride, ix.dstride * 4u);
+            }
         }
 
         // ---- projection table (projection.cpp:123-137), serial dot per entry
@@ -1868,6 +1813,7 @@ __global__ void __launch_bounds__(128, PAG_MIN_BLOCKS) pag_search_kernel(const _
             }
         }
         __syncwarp();
+        if (EXACT) interleave_query(c.q, ix.padded, ix.xstride, lane);
 
         for (int g = 0; g < 2; ++g) {
             if (!seed_sel[g]) continue;

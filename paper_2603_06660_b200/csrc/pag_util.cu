@@ -39,7 +39,35 @@ __global__ void dup_groups_kernel(const uint8_t* __restrict__ adj, const uint32_
     }
 }
 
+// rows -> the chain-interleaved copy (pag_device.h chain_positions): one
+// thread per output float; a row's reads stay inside its own lines
+__global__ void interleave_rows_kernel(const float* __restrict__ rows, float* __restrict__ rowsX, uint64_t first,
+                                       uint64_t n, uint32_t padded, uint32_t dstride, uint32_t xstride) {
+    const uint32_t D4 = padded & ~3u, P = D4 >> 2;
+    const uint64_t total = (n - first) * xstride;
+    for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+         t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t row = first + t / xstride;
+        const uint32_t xi = static_cast<uint32_t>(t % xstride);
+        const uint32_t c = (xi >> 3) & 3u, p = ((xi >> 5) << 3) + (xi & 7u);
+        float v = 0.0f;
+        if (p < P)
+            v = rows[row * dstride + 4u * p + c];
+        else if (c == 0 && D4 + (p - P) < padded)
+            v = rows[row * dstride + D4 + (p - P)];
+        rowsX[row * xstride + xi] = v;
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_interleave_rows(const float* rows, float* rowsX, uint64_t first, uint64_t n, uint32_t padded,
+                                   uint32_t dstride, cudaStream_t stream) {
+    if (n <= first) return cudaSuccess;
+    interleave_rows_kernel<<<148 * 16, 256, 0, stream>>>(rows, rowsX, first, n, padded, dstride,
+                                                          chain_xstride(padded));
+    return cudaGetLastError();
+}
 
 cudaError_t count_dup_groups(const void* adj, const uint32_t* deg, uint64_t n, uint32_t block_bytes,
                              uint32_t* count_dev, cudaStream_t stream) {
