@@ -56,7 +56,9 @@ typedef struct pag_search_params {
     uint8_t use_prt;     /* ablation: 0 degenerates to exact expansion */
     uint8_t use_tfb;     /* ablation: 0 = one round with b = max(efS, b) */
     uint8_t exact_dist;  /* 1 (default): reference-order fp32 sq_dist, bit-identical
-                            results; 0: warp-tree FMA distances (within 1e-5 rel) */
+                            results (the first such search builds a second,
+                            chain-interleaved copy of the rows in HBM);
+                            0: warp-tree FMA distances (within 1e-5 rel) */
     uint8_t reserved;
 } pag_search_params;
 
@@ -84,7 +86,8 @@ int pag_gpu_open_devices(const char* index_path, const int* devices, uint32_t n_
 int pag_gpu_close(pag_gpu_index* ix);
 
 /* info[0..11] = n, dim, padded_dim, L, m, M, metric (0 euclidean, 1 cosine),
- * n_entries, seed, total_edges, n_devices, device_bytes_per_replica;
+ * n_entries, seed, total_edges, n_devices, device_bytes_per_replica (grows
+ * by one more copy of the rows at the first reference-order search);
  * info[12] = tensor-core ground-truth queries re-run exactly so far;
  * info[13..15] = the header's efC, b_build, enable_pes;
  * info[16] = nodes that repeat a target inside one 32-edge group (0 lets

@@ -1705,7 +1705,10 @@ int pag_gpu_info(const pag_gpu_index* ix, uint64_t* info, size_t n_info) {
         if (!ix || !info) throw_err(PAG_GPU_EINVAL, "null argument");
         const uint64_t v[17] = {ix->n, ix->dim, ix->padded, ix->L, ix->m, ix->M, ix->metric,
                                 ix->entries.size(), ix->seed, ix->total_edges, ix->reps.size(),
-                                ix->reps.empty() ? 0 : ix->reps[0].bytes, ix->gt_uncertified,
+                                ix->reps.empty() ? 0
+                                                 : ix->reps[0].bytes + ix->reps[0].rows_x_cap * 4ull *
+                                                                           pagdev::chain_xstride(ix->padded),
+                                ix->gt_uncertified,
                                 ix->efC, ix->b_build, ix->enable_pes, ix->dup_nodes};
         for (size_t i = 0; i < n_info && i < 17; ++i) info[i] = v[i];
     });

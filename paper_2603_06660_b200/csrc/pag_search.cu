@@ -1119,7 +1119,8 @@ __device__ __forceinline__ F8 ldg_f8(const float* p) {
 
 template <int NLN>
 __device__ void dist_exact_x(const SearchLaunch& P, Common& c, uint32_t items, uint32_t w, int lane) {
-    constexpr int LA = NLN ? (PAG_OCC >= 6 ? 3 : 6) : 2;  // lines in flight per lane (register budget)
+    // lines in flight per lane (register budget; cfg-2: 4 / 6 / 8 / 12 -> 2.30 / 2.23 / 2.33 / 2.35 ms)
+    constexpr int LA = NLN ? (PAG_OCC >= 6 ? 3 : 6) : 2;
     const IndexView& ix = P.ix;
     const uint32_t XS = NLN ? 32u * NLN : ix.xstride;
     const uint32_t nln = NLN ? NLN : XS / 32u;
@@ -1593,11 +1594,12 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
         // marks of this group's passes (routing.cpp:183). Later lookups come
         // from the next group/expansion only (in-group duplicates are resolved
         // by `same`), so the inserts are deferred and done in parallel.
+        PT(6);
         if (passed) mark_many(c, passed, w, lane);
         // a copy skipped after an earlier copy in the group passed is no test
         c.n_test += __popc(cand_mask);
         if (any_dup) c.n_test -= __popc(__ballot_sync(FULL, cand && ((same & lt & passed) != 0u)));
-        PT(6);
+        PT(1);
         __syncwarp();
     }
     return track_pes && !pes_ok;

@@ -43,6 +43,11 @@ def test_refresh_matches_oracle_each_phase(phases):
     idx, files, q = phases
     ix = pag.load_index(idx)
     try:
+        # a reference-order search before the first refresh: the chain-interleaved
+        # row copy exists already and every refresh has to extend it
+        got = ix.search_batch(q, pag.SearchParams(K=10, efS=40))
+        want = O.OracleIndex(idx).search(q, 10, 40)
+        assert_same_results((got.ids, got.sq, got.n_out, got.stats), want, idx)
         for path in files:
             st = ix.refresh(path)
             assert st["new_nodes"] == 150 and 150 <= st["changed_blocks"] < ix.n

@@ -29,7 +29,7 @@ fn(buf, 1)
 r = ix.search_batch(q, params)
 fn(buf, 1)
 buf = list(buf)
-names = ["setup+T+seeds", "-", "argmin/entry/adj-issue", "adjacency wait+visited", "PRT+codes",
+names = ["setup+T+seeds", "marks", "argmin/entry/adj-issue", "adjacency wait+visited", "PRT+codes",
          "distances", "replay", "end_round/flush/out"]
 tot = sum(buf)
 exp = r.stats[:, 3].sum()
