@@ -82,6 +82,44 @@ int pag_gpu_open(const char* index_path, uint32_t device_mask, pag_gpu_index** o
  * replica; the others are filled device to device. n_devices = 0 = {0}. */
 int pag_gpu_open_devices(const char* index_path, const int* devices, uint32_t n_devices, pag_gpu_index** out);
 
+/* The reference's in-memory PagIndex (proj/include/pag/builder.hpp:62-132),
+ * borrowed for the duration of a call: the source of pag_gpu_open_from_arrays
+ * and pag_gpu_refresh_from_arrays, so an index the reference has just built
+ * or extended (build / insert_online) reaches the GPU without a file.
+ *   header        BuildParams (builder.hpp:27-36) + VectorSet dim / padded_dim / metric
+ *   degrees       n x u32, a snapshot of PagIndex::degree(u) (:74-76; atomics there)
+ *   targets       n x 2M u32, PagIndex::targets(0) (:77-79, fixed stride 2M)
+ *   scalars       n x 2M x {cos_beta, edge_norm, base_offset} f32, scalars(0) (:38-42,80-82)
+ *   codes         n x 2M x ceil(L/2) bytes, edge_codes(0, 0) (:83-85)
+ *   rows          n x padded_dim f32, vectors().row(0) (vecstore.hpp:38)
+ *   norms         n cached norms (vecstore.hpp:39) or NULL (computed from the rows)
+ * L is the resolved subspace count (refs().L), or 0 for the dimension default. */
+typedef struct pag_index_arrays {
+    uint64_t n;
+    uint32_t dim, padded_dim, L, m, M, efC, b_build, pes_flush_interval;
+    uint64_t seed;
+    uint8_t metric;      /* 0 euclidean, 1 cosine */
+    uint8_t enable_pes;
+    uint8_t reserved[2];
+    uint32_t n_entries;
+    const uint32_t* entry_nodes;
+    const uint32_t* degrees;
+    const uint32_t* targets;
+    const float* scalars;
+    const uint8_t* codes;
+    const float* rows;
+    const float* norms;
+} pag_index_arrays;
+
+/* pag_gpu_open_devices with the in-memory arrays as the source (same
+ * validation and errors as the file path; nothing of `a` is kept). */
+int pag_gpu_open_from_arrays(const pag_index_arrays* a, const int* devices, uint32_t n_devices,
+                             pag_gpu_index** out);
+
+/* pag_gpu_refresh with the in-memory arrays as the newer state (after
+ * insert_online batches on the PagIndex the GPU index was opened from). */
+int pag_gpu_refresh_from_arrays(pag_gpu_index* ix, const pag_index_arrays* a, uint64_t* stats);
+
 /* Releases every device replica (the PagIndex destructor). */
 int pag_gpu_close(pag_gpu_index* ix);
 

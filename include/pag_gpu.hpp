@@ -4,6 +4,7 @@
 // reference's types onto the ABI:
 //   SearchParams / SearchResult / Candidate   proj/include/pag/routing.hpp:13-34,173-177
 //   PagIndex load_index(const std::string&)   proj/include/pag/builder.hpp:157
+//   PagIndex (in memory, after build / insert_online)  builder.hpp:62-132
 //   search(const PagIndex&, span, SearchParams, TfbState&)  routing.hpp:181-184
 // and the ABI's status codes onto the reference's exception classes
 // (std::invalid_argument / std::runtime_error, same message texts).
@@ -27,17 +28,76 @@ inline void gpu_check(int rc) {
     throw std::runtime_error(msg);
 }
 
-// A PAGIDX01 index resident on one or more GPUs (move-only, like PagIndex).
+// The reference's in-memory PagIndex as the ABI's borrowed arrays
+// (pag_index_arrays): fixed-stride accessors of builder.hpp:74-85, a
+// snapshot of the atomic degrees; norms are recomputed from the rows.
+struct IndexArrays {
+    pag_index_arrays a{};
+    std::vector<uint32_t> degrees;
+    explicit IndexArrays(const PagIndex& ix) : degrees(ix.size()) {
+        static_assert(sizeof(EdgeScalars) == 3 * sizeof(float), "EdgeScalars is {cos_beta, edge_norm, base_offset}");
+        for (uint32_t u = 0; u < ix.size(); ++u) degrees[u] = ix.degree(u);
+        const BuildParams& bp = ix.params();
+        a.n = ix.size();
+        a.dim = static_cast<uint32_t>(ix.vectors().dim());
+        a.padded_dim = static_cast<uint32_t>(ix.vectors().padded_dim());
+        a.L = ix.refs().L;
+        a.m = bp.m;
+        a.M = bp.M;
+        a.efC = bp.efC;
+        a.b_build = bp.b_build;
+        a.pes_flush_interval = bp.pes_flush_interval;
+        a.seed = bp.seed;
+        a.metric = static_cast<uint8_t>(ix.vectors().metric());
+        a.enable_pes = bp.enable_pes ? 1 : 0;
+        a.n_entries = static_cast<uint32_t>(ix.entry_nodes().size());
+        a.entry_nodes = ix.entry_nodes().data();
+        a.degrees = degrees.data();
+        if (ix.size()) {
+            a.targets = ix.targets(0);
+            a.scalars = reinterpret_cast<const float*>(ix.scalars(0));
+            a.codes = ix.edge_codes(0, 0);
+            a.rows = ix.vectors().row(0);
+        }
+        a.norms = nullptr;
+    }
+};
+
+// A PAG index resident on one or more GPUs (move-only, like PagIndex): from
+// a PAGIDX01 file, or straight from the reference's in-memory PagIndex.
 class GpuIndex {
 public:
+    explicit GpuIndex(const PagIndex& index, std::vector<int> devices = {0}) {
+        const IndexArrays ia(index);
+        gpu_check(pag_gpu_open_from_arrays(&ia.a, devices.data(), static_cast<uint32_t>(devices.size()), &h_));
+        read_info();
+    }
     explicit GpuIndex(const std::string& path, std::vector<int> devices = {0}) {
         gpu_check(pag_gpu_open_devices(path.c_str(), devices.data(), static_cast<uint32_t>(devices.size()), &h_));
+        read_info();
+    }
+    // re-synchronise with the PagIndex after insert_online batches (only new
+    // rows and changed adjacency blocks travel)
+    void refresh(const PagIndex& index) {
+        const IndexArrays ia(index);
+        gpu_check(pag_gpu_refresh_from_arrays(h_, &ia.a, nullptr));
+        read_info();
+    }
+    void refresh(const std::string& path) {
+        gpu_check(pag_gpu_refresh(h_, path.c_str(), nullptr));
+        read_info();
+    }
+
+private:
+    void read_info() {
         uint64_t info[17];
         gpu_check(pag_gpu_info(h_, info, 17));
         n_ = info[0];
         dim_ = static_cast<uint32_t>(info[1]);
         efC_ = static_cast<uint32_t>(info[13]);
     }
+
+public:
     GpuIndex(GpuIndex&& o) noexcept : h_(o.h_), n_(o.n_), dim_(o.dim_), efC_(o.efC_) { o.h_ = nullptr; }
     GpuIndex(const GpuIndex&) = delete;
     GpuIndex& operator=(const GpuIndex&) = delete;

@@ -13,7 +13,7 @@ from __future__ import annotations
 
 import importlib
 
-__all__ = ["BatchResult", "ConstructionResult", "PagIndex", "PendingBatch", "SearchParams", "SearchResult",
+__all__ = ["BatchResult", "ConstructionResult", "IndexArrays", "PagIndex", "PendingBatch", "SearchParams", "SearchResult",
            "SearchStats", "ground_truth", "load_index", "mean_recall", "recall_at_k", "search"]
 
 

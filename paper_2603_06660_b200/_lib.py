@@ -26,6 +26,8 @@ EXPORTS = (
     "pag_gpu_default_params",
     "pag_gpu_open",
     "pag_gpu_open_devices",
+    "pag_gpu_open_from_arrays",
+    "pag_gpu_refresh_from_arrays",
     "pag_gpu_close",
     "pag_gpu_info",
     "pag_gpu_search",
@@ -57,6 +59,16 @@ class SearchParamsC(C.Structure):
                 ("reserved", C.c_uint8)]
 
 
+class IndexArraysC(C.Structure):
+    """pag_index_arrays: the reference's in-memory PagIndex, borrowed for a call."""
+    _fields_ = [("n", C.c_uint64), ("dim", C.c_uint32), ("padded_dim", C.c_uint32), ("L", C.c_uint32),
+                ("m", C.c_uint32), ("M", C.c_uint32), ("efC", C.c_uint32), ("b_build", C.c_uint32),
+                ("pes_flush_interval", C.c_uint32), ("seed", C.c_uint64), ("metric", C.c_uint8),
+                ("enable_pes", C.c_uint8), ("reserved", C.c_uint8 * 2), ("n_entries", C.c_uint32),
+                ("entry_nodes", C.c_void_p), ("degrees", C.c_void_p), ("targets", C.c_void_p),
+                ("scalars", C.c_void_p), ("codes", C.c_void_p), ("rows", C.c_void_p), ("norms", C.c_void_p)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -71,6 +83,9 @@ def _load():
         "pag_gpu_default_params": (None, [C.POINTER(SearchParamsC)]),
         "pag_gpu_open": (C.c_int, [C.c_char_p, C.c_uint32, C.POINTER(P)]),
         "pag_gpu_open_devices": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.c_uint32, C.POINTER(P)]),
+        "pag_gpu_open_from_arrays": (C.c_int, [C.POINTER(IndexArraysC), C.POINTER(C.c_int), C.c_uint32,
+                                               C.POINTER(P)]),
+        "pag_gpu_refresh_from_arrays": (C.c_int, [P, C.POINTER(IndexArraysC), u64p]),
         "pag_gpu_close": (C.c_int, [P]),
         "pag_gpu_info": (C.c_int, [P, u64p, C.c_size_t]),
         "pag_gpu_search": (C.c_int, [P, C.c_void_p, C.c_uint64, C.POINTER(SearchParamsC),

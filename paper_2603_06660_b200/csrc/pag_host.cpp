@@ -403,6 +403,52 @@ void fill_block(uint8_t* blk, const uint8_t* e, uint32_t deg, uint64_t n, uint32
 // dry = true: parse and validate the whole file on the host only (no GPU).
 // devs: one replica per entry (a device may repeat: several replicas on one
 // GPU, each with its own copy, stream and scratch)
+// header fields -> validation (builder.cpp:434-446) and the derived device
+// layout; regenerates the reference family
+void init_layout(pag_gpu_index& ix) {
+    if (ix.n >= 0xFFFFFFFFull) throw_err(PAG_GPU_ERUNTIME, "index too large for 32-bit ids");
+    // PagIndex constructor: VectorSet(dim, padded) then repad(L) (builder.cpp:40-46)
+    if (ix.padded < ix.dim) throw_err(PAG_GPU_EINVAL, "padded_dim < dim");
+    if (ix.L == 0) ix.L = default_L(ix.dim);
+    if (((ix.dim + ix.L - 1) / ix.L) * ix.L != ix.padded)
+        throw_err(PAG_GPU_ERUNTIME, "padded_dim mismatch on load");
+    ix.refs = reference_family(ix.padded, ix.L, ix.m, ix.seed);
+    ix.sub_dim = ix.padded / ix.L;
+    ix.dstride = (ix.padded + 3u) & ~3u;
+    ix.maxdeg = 2 * ix.M;
+    ix.cb = (ix.L + 1) / 2;
+    ix.cwp = 1;
+    while (ix.cwp * 4 < ix.cb) ix.cwp *= 2;
+    ix.slot_stride = std::max(32u, (ix.maxdeg + 31u) & ~31u);
+    ix.block_bytes = ix.slot_stride * (16u + 4u * ix.cwp);
+}
+
+// Where an index comes from: node(u, blk) fills node u's zeroed device block
+// and returns its degree (called for u = 0 .. n-1 in order); rows() / norms()
+// give the n x padded_dim rows and the n cached norms (norms may be null:
+// computed from the rows), valid once every node has been read.
+struct IndexSource {
+    std::function<uint32_t(uint64_t, uint8_t*)> node;
+    std::function<const uint8_t*()> rows;
+    std::function<const uint8_t*()> norms;
+};
+
+// vecstore.cpp:97-108 (the cached norm of a stored row), for sources without norms
+float host_vec_norm(const float* a, size_t padded) {
+    float acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+    size_t k = 0;
+    for (; k + 4 <= padded; k += 4) {
+        acc0 += a[k] * a[k];
+        acc1 += a[k + 1] * a[k + 1];
+        acc2 += a[k + 2] * a[k + 2];
+        acc3 += a[k + 3] * a[k + 3];
+    }
+    for (; k < padded; ++k) acc0 += a[k] * a[k];
+    return std::sqrt((acc0 + acc1) + (acc2 + acc3));
+}
+
+void upload_index(pag_gpu_index* ix, const std::vector<int>& devs, bool dry, const IndexSource& src);
+
 std::unique_ptr<pag_gpu_index> open_index(const char* path, const std::vector<int>& devs, bool dry = false) {
     Mapped mp;
     mp.fd = ::open(path, O_RDONLY);
@@ -435,22 +481,35 @@ std::unique_ptr<pag_gpu_index> open_index(const char* path, const std::vector<in
     const uint32_t n_entries = cur.pod<uint32_t>();
     ix->entries.resize(n_entries);
     if (n_entries) std::memcpy(ix->entries.data(), cur.take(4ull * n_entries), 4ull * n_entries);
-    if (ix->n >= 0xFFFFFFFFull) throw_err(PAG_GPU_ERUNTIME, "index too large for 32-bit ids");
-    // PagIndex constructor: VectorSet(dim, padded) then repad(L) (builder.cpp:40-46)
-    if (ix->padded < ix->dim) throw_err(PAG_GPU_EINVAL, "padded_dim < dim");
-    if (ix->L == 0) ix->L = default_L(ix->dim);
-    if (((ix->dim + ix->L - 1) / ix->L) * ix->L != ix->padded)
-        throw_err(PAG_GPU_ERUNTIME, "padded_dim mismatch on load");
-    ix->refs = reference_family(ix->padded, ix->L, ix->m, ix->seed);
-    ix->sub_dim = ix->padded / ix->L;
-    ix->dstride = (ix->padded + 3u) & ~3u;
-    ix->maxdeg = 2 * ix->M;
-    ix->cb = (ix->L + 1) / 2;
-    ix->cwp = 1;
-    while (ix->cwp * 4 < ix->cb) ix->cwp *= 2;
-    ix->slot_stride = std::max(32u, (ix->maxdeg + 31u) & ~31u);
-    ix->block_bytes = ix->slot_stride * (16u + 4u * ix->cwp);
+    init_layout(*ix);
+    // file records in node order, then the rows and the cached norms
+    const uint64_t n = ix->n;
+    const uint32_t S = ix->slot_stride, cb = ix->cb, cwp = ix->cwp, maxdeg = ix->maxdeg, padded = ix->padded;
+    const size_t rec = 4 + cb + 12;
+    const uint8_t* rows_p = nullptr;
+    IndexSource src;
+    src.node = [&](uint64_t, uint8_t* blk) {
+        const uint32_t deg = cur.pod<uint32_t>();
+        if (deg > maxdeg) throw_err(PAG_GPU_ERUNTIME, "degree over cap in file");
+        fill_block(blk, cur.take(rec * deg), deg, n, S, cb, cwp);
+        return deg;
+    };
+    src.rows = [&] {
+        rows_p = cur.take(4ull * padded * n);
+        cur.take(4ull * n);  // cached norms (presence checked here)
+        return rows_p;
+    };
+    src.norms = [&] { return rows_p + 4ull * padded * n; };
+    upload_index(ix.get(), devs, dry, src);
+    return ix;
+}
 
+// source -> device layout on every replica of devs
+// dry = true: parse and validate the whole source on the host only (no GPU).
+// devs: one replica per entry (a device may repeat: several replicas on one
+// GPU, each with its own copy, stream and scratch)
+void upload_index(pag_gpu_index* ix, const std::vector<int>& devs, bool dry, const IndexSource& src) {
+    const uint32_t n_entries = static_cast<uint32_t>(ix->entries.size());
     if (!dry) {
         if (devs.empty()) throw_err(PAG_GPU_EINVAL, "no device given");
         int ndev = 0;
@@ -533,10 +592,8 @@ std::unique_ptr<pag_gpu_index> open_index(const char* path, const std::vector<in
             }
         }
     } fr{stage, dstage, dry};
-    const uint32_t S = ix->slot_stride, cb = ix->cb, cwp = ix->cwp;
-    const size_t rec = 4 + cb + 12;
     int buf = 0;
-    // the file streams through pinned staging into the first replica; the
+    // the source streams through pinned staging into the first replica; the
     // others are then filled device to device (NVLink peer copies across
     // GPUs, or on-device copies), so the host link carries the index once
     Replica* r0 = ix->reps.empty() ? nullptr : &ix->reps[0];
@@ -547,11 +604,9 @@ std::unique_ptr<pag_gpu_index> open_index(const char* path, const std::vector<in
         uint32_t* dg = dstage[buf];
         std::memset(blk0, 0, cnt * ix->block_bytes);
         for (uint64_t i = 0; i < cnt; ++i) {
-            const uint32_t deg = cur.pod<uint32_t>();
-            if (deg > ix->maxdeg) throw_err(PAG_GPU_ERUNTIME, "degree over cap in file");
+            const uint32_t deg = src.node(u0 + i, blk0 + i * ix->block_bytes);
             dg[i] = deg;
             ix->total_edges += deg;
-            fill_block(blk0 + i * ix->block_bytes, cur.take(rec * deg), deg, n, S, cb, cwp);
         }
         if (r0) {
             cudaSetDevice(r0->device);
@@ -567,8 +622,8 @@ std::unique_ptr<pag_gpu_index> open_index(const char* path, const std::vector<in
 
     // rows (n x padded fp32), restrided to dstride with zero padding
     {
-        const uint8_t* rows = cur.take(4ull * ix->padded * n);
-        cur.take(4ull * n);  // cached norms: read (presence checked) but not needed on device
+        const uint8_t* rows = src.rows();
+        const uint8_t* norms = src.norms();
         const size_t RCH = std::max<size_t>(1, chunk_bytes / row_bytes);
         buf = 0;
         for (uint64_t i0 = 0; i0 < n; i0 += RCH) {
@@ -608,10 +663,12 @@ std::unique_ptr<pag_gpu_index> open_index(const char* path, const std::vector<in
         // stored rows' vec_norm, builder.cpp:489-491)
         if (!ix->reps.empty()) {
             std::vector<float> bn(n);
-            const uint8_t* norms = rows + 4ull * ix->padded * n;
             for (uint64_t i = 0; i < n; ++i) {
                 float v;
-                std::memcpy(&v, norms + 4 * i, 4);
+                if (norms)
+                    std::memcpy(&v, norms + 4 * i, 4);
+                else
+                    v = host_vec_norm(reinterpret_cast<const float*>(rows) + i * ix->padded, ix->padded);
                 bn[i] = v * v;
                 ix->max_bnorm = std::max(ix->max_bnorm, bn[i]);
             }
@@ -622,7 +679,6 @@ std::unique_ptr<pag_gpu_index> open_index(const char* path, const std::vector<in
             }
         }
     }
-    return ix;
 }
 
 // ---------------------------------------------------------------------------
@@ -1220,38 +1276,33 @@ void grow_replica(pag_gpu_index& ix, Replica& r, uint64_t need) {
     r.cap_nodes = cap;
 }
 
-void refresh_index(pag_gpu_index& ix, const char* path, uint64_t* st) {
+// A newer state of the loaded index: header fields to check, random-access
+// node records (thread-safe: called from several host threads), rows, norms.
+struct RefreshSource {
+    uint64_t n_new = 0;
+    uint32_t dim = 0, padded = 0, L = 0, m = 0, M = 0;
+    uint64_t seed = 0;
+    uint8_t metric = 0;
+    const uint32_t* entries = nullptr;
+    uint32_t n_entries = 0;
+    std::function<uint32_t(uint64_t)> degree;              // deg(u)
+    std::function<void(uint64_t, uint32_t, uint8_t*)> fill;  // node u with deg edges -> zeroed block
+    const uint8_t* rows = nullptr;   // n_new x padded fp32
+    const uint8_t* norms = nullptr;  // n_new cached norms, or null (computed)
+};
+
+void refresh_from(pag_gpu_index& ix, const RefreshSource& src, uint64_t* st) {
     const auto t0 = std::chrono::steady_clock::now();
-    Mapped mp;
-    mp.fd = ::open(path, O_RDONLY);
-    if (mp.fd < 0) throw_err(PAG_GPU_ERUNTIME, std::string("cannot open index: ") + path);
-    struct stat sb;
-    if (fstat(mp.fd, &sb) != 0 || sb.st_size == 0) throw_err(PAG_GPU_ERUNTIME, "index read failed");
-    mp.size = static_cast<size_t>(sb.st_size);
-    void* mm = mmap(nullptr, mp.size, PROT_READ, MAP_PRIVATE, mp.fd, 0);
-    if (mm == MAP_FAILED) throw_err(PAG_GPU_ERUNTIME, std::string("cannot open index: ") + path);
-    mp.p = static_cast<const uint8_t*>(mm);
-    Cursor cur{mp.p, mp.size};
-    if (cur.pod<uint64_t>() != 0x5041474944583031ull) throw_err(PAG_GPU_ERUNTIME, "bad index magic");
-    if (cur.pod<uint32_t>() != 1u) throw_err(PAG_GPU_ERUNTIME, "unsupported index version");
-    const uint64_t n_new = cur.pod<uint64_t>();
-    const uint32_t dim = cur.pod<uint32_t>(), padded = cur.pod<uint32_t>(), L = cur.pod<uint32_t>(),
-                   m = cur.pod<uint32_t>(), M = cur.pod<uint32_t>();
-    cur.pod<uint32_t>();  // efC
-    cur.pod<uint32_t>();  // b_build
-    cur.pod<uint32_t>();  // pes_flush_interval
-    const uint64_t seed = cur.pod<uint64_t>();
-    const uint8_t metric = cur.pod<uint8_t>();
-    cur.pod<uint8_t>();
-    const uint32_t ne = cur.pod<uint32_t>();
-    const uint8_t* ent = cur.take(4ull * ne);
-    if (dim != ix.dim || padded != ix.padded || (L != ix.L && L != 0) || m != ix.m || M != ix.M ||
-        seed != ix.seed || metric != ix.metric || n_new < ix.n || ne != ix.entries.size() ||
-        (ne && std::memcmp(ent, ix.entries.data(), 4ull * ne) != 0))
+    const uint64_t n_new = src.n_new;
+    const uint32_t padded = src.padded;
+    if (src.dim != ix.dim || padded != ix.padded || (src.L != ix.L && src.L != 0) || src.m != ix.m ||
+        src.M != ix.M || src.seed != ix.seed || src.metric != ix.metric || n_new < ix.n ||
+        src.n_entries != ix.entries.size() ||
+        (src.n_entries && std::memcmp(src.entries, ix.entries.data(), 4ull * src.n_entries) != 0))
         throw_err(PAG_GPU_EINVAL, "refresh: index is not an extension of the loaded one");
+    if (n_new >= 0xFFFFFFFFull) throw_err(PAG_GPU_ERUNTIME, "index too large for 32-bit ids");
     const uint64_t n_old = ix.n;
-    const uint32_t BB = ix.block_bytes, S = ix.slot_stride, cb = ix.cb, cwp = ix.cwp;
-    const size_t rec = 4 + cb + 12;
+    const uint32_t BB = ix.block_bytes;
     Replica& r0 = ix.reps.at(0);
     cudaSetDevice(r0.device);
     if (ix.mirror_deg.size() != n_old) {  // first refresh: mirror the device state
@@ -1262,18 +1313,15 @@ void refresh_index(pag_gpu_index& ix, const char* path, uint64_t* st) {
     }
     ix.mirror_adj.resize(n_new * BB);
     ix.mirror_deg.resize(n_new);
-    // pass 1 (sequential): record offsets and degrees; pass 2 (host threads
-    // over node ranges): build each block, diff it against the mirror and
-    // collect the changed ones (merged in node order)
-    std::vector<uint64_t> recoff(n_new);
+    // host threads over node ranges: build each block, diff it against the
+    // mirror and collect the changed ones (merged in node order)
     std::vector<uint32_t> degs(n_new);
     uint64_t edges = 0;
     for (uint64_t u = 0; u < n_new; ++u) {
-        const uint32_t deg = cur.pod<uint32_t>();
+        const uint32_t deg = src.degree(u);
         if (deg > ix.maxdeg) throw_err(PAG_GPU_ERUNTIME, "degree over cap in file");
         edges += deg;
         degs[u] = deg;
-        recoff[u] = static_cast<uint64_t>(cur.take(rec * deg) - mp.p);
     }
     const unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
     std::vector<std::vector<uint32_t>> dirty_t(nth);
@@ -1284,7 +1332,7 @@ void refresh_index(pag_gpu_index& ix, const char* path, uint64_t* st) {
         try {
             for (uint64_t u = u0; u < u1; ++u) {
                 std::fill(blk.begin(), blk.end(), 0);
-                fill_block(blk.data(), mp.p + recoff[u], degs[u], n_new, S, cb, cwp);
+                src.fill(u, degs[u], blk.data());
                 uint8_t* mb = &ix.mirror_adj[u * BB];
                 if (u >= n_old || ix.mirror_deg[u] != degs[u] || std::memcmp(mb, blk.data(), BB) != 0) {
                     std::memcpy(mb, blk.data(), BB);
@@ -1306,15 +1354,18 @@ void refresh_index(pag_gpu_index& ix, const char* path, uint64_t* st) {
         if (!e.empty()) throw_err(PAG_GPU_ERUNTIME, e);
     std::vector<uint32_t> dirty;
     for (const auto& d : dirty_t) dirty.insert(dirty.end(), d.begin(), d.end());
-    const uint8_t* rows = cur.take(4ull * padded * n_new);
-    const uint8_t* norms = cur.take(4ull * n_new);
+    const uint8_t* rows = src.rows;
+    const uint8_t* norms = src.norms;
     const size_t row_bytes = 4ull * ix.dstride;
     std::vector<uint8_t> newrows((n_new - n_old) * row_bytes, 0);
     std::vector<float> newbn(n_new - n_old);
     for (uint64_t i = n_old; i < n_new; ++i) {
         std::memcpy(&newrows[(i - n_old) * row_bytes], rows + i * 4ull * padded, 4ull * padded);
         float v;
-        std::memcpy(&v, norms + 4 * i, 4);
+        if (norms)
+            std::memcpy(&v, norms + 4 * i, 4);
+        else
+            v = host_vec_norm(reinterpret_cast<const float*>(rows) + i * padded, padded);
         newbn[i - n_old] = v * v;
         ix.max_bnorm = std::max(ix.max_bnorm, newbn[i - n_old]);
     }
@@ -1355,6 +1406,143 @@ void refresh_index(pag_gpu_index& ix, const char* path, uint64_t* st) {
         st[3] = static_cast<uint64_t>(
             std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
     }
+}
+
+void refresh_index(pag_gpu_index& ix, const char* path, uint64_t* st) {
+    Mapped mp;
+    mp.fd = ::open(path, O_RDONLY);
+    if (mp.fd < 0) throw_err(PAG_GPU_ERUNTIME, std::string("cannot open index: ") + path);
+    struct stat sb;
+    if (fstat(mp.fd, &sb) != 0 || sb.st_size == 0) throw_err(PAG_GPU_ERUNTIME, "index read failed");
+    mp.size = static_cast<size_t>(sb.st_size);
+    void* mm = mmap(nullptr, mp.size, PROT_READ, MAP_PRIVATE, mp.fd, 0);
+    if (mm == MAP_FAILED) throw_err(PAG_GPU_ERUNTIME, std::string("cannot open index: ") + path);
+    mp.p = static_cast<const uint8_t*>(mm);
+    Cursor cur{mp.p, mp.size};
+    if (cur.pod<uint64_t>() != 0x5041474944583031ull) throw_err(PAG_GPU_ERUNTIME, "bad index magic");
+    if (cur.pod<uint32_t>() != 1u) throw_err(PAG_GPU_ERUNTIME, "unsupported index version");
+    RefreshSource src;
+    src.n_new = cur.pod<uint64_t>();
+    src.dim = cur.pod<uint32_t>();
+    src.padded = cur.pod<uint32_t>();
+    src.L = cur.pod<uint32_t>();
+    src.m = cur.pod<uint32_t>();
+    src.M = cur.pod<uint32_t>();
+    cur.pod<uint32_t>();  // efC
+    cur.pod<uint32_t>();  // b_build
+    cur.pod<uint32_t>();  // pes_flush_interval
+    src.seed = cur.pod<uint64_t>();
+    src.metric = cur.pod<uint8_t>();
+    cur.pod<uint8_t>();
+    src.n_entries = cur.pod<uint32_t>();
+    src.entries = reinterpret_cast<const uint32_t*>(cur.take(4ull * src.n_entries));
+    // the file is scanned once for record offsets and degrees
+    const uint64_t n_new = src.n_new;
+    if (n_new < ix.n || src.padded != ix.padded || src.M != ix.M || (src.L != ix.L && src.L != 0))
+        throw_err(PAG_GPU_EINVAL, "refresh: index is not an extension of the loaded one");
+    const uint32_t S = ix.slot_stride, cb = ix.cb, cwp = ix.cwp;
+    const size_t rec = 4 + cb + 12;
+    std::vector<uint64_t> recoff(n_new);
+    std::vector<uint32_t> degs(n_new);
+    for (uint64_t u = 0; u < n_new; ++u) {
+        const uint32_t deg = cur.pod<uint32_t>();
+        if (deg > ix.maxdeg) throw_err(PAG_GPU_ERUNTIME, "degree over cap in file");
+        degs[u] = deg;
+        recoff[u] = static_cast<uint64_t>(cur.take(rec * deg) - mp.p);
+    }
+    src.degree = [&](uint64_t u) { return degs[u]; };
+    src.fill = [&](uint64_t u, uint32_t deg, uint8_t* blk) { fill_block(blk, mp.p + recoff[u], deg, n_new, S, cb, cwp); };
+    src.rows = cur.take(4ull * src.padded * n_new);
+    src.norms = cur.take(4ull * n_new);
+    refresh_from(ix, src, st);
+}
+
+// ---------------------------------------------------------------------------
+// The reference's in-memory PagIndex as the source (pag_index_arrays,
+// builder.hpp:62-132): fixed-stride targets / scalars / codes, a copy of the
+// degrees, the VectorSet's rows and norms. Same validation as the file path.
+// ---------------------------------------------------------------------------
+void check_arrays(const pag_index_arrays* a) {
+    if (!a) throw_err(PAG_GPU_EINVAL, "null argument");
+    if (a->n && (!a->degrees || !a->targets || !a->scalars || !a->codes || !a->rows))
+        throw_err(PAG_GPU_EINVAL, "null argument");
+    if (a->n_entries && !a->entry_nodes) throw_err(PAG_GPU_EINVAL, "null argument");
+}
+
+// node u of the arrays -> the device block (zeroed by the caller)
+void fill_block_arrays(uint8_t* blk, const pag_index_arrays& a, uint64_t u, uint32_t deg, uint64_t n, uint32_t S,
+                       uint32_t cb, uint32_t cwp) {
+    const uint64_t stride = 2ull * a.M;  // PagIndex::max_degree (builder.hpp:72)
+    const uint32_t* tg_in = a.targets + u * stride;
+    const float* sc = a.scalars + 3ull * u * stride;  // EdgeScalars{cos_beta, edge_norm, base_offset}
+    const uint8_t* cd = a.codes + u * stride * cb;
+    uint32_t* tg = reinterpret_cast<uint32_t*>(blk);
+    float* en = reinterpret_cast<float*>(blk + 4u * S);
+    float* cbeta = reinterpret_cast<float*>(blk + 8u * S);
+    float* bo = reinterpret_cast<float*>(blk + 12u * S);
+    uint8_t* codes = blk + 16u * S;
+    for (uint32_t j = 0; j < deg; ++j) {
+        if (tg_in[j] >= n) throw_err(PAG_GPU_ERUNTIME, "edge target out of range in file");
+        tg[j] = tg_in[j];
+        std::memcpy(codes + static_cast<size_t>(j) * 4 * cwp, cd + static_cast<size_t>(j) * cb, cb);
+        cbeta[j] = sc[3 * j];
+        en[j] = sc[3 * j + 1];
+        bo[j] = sc[3 * j + 2];
+    }
+}
+
+std::unique_ptr<pag_gpu_index> open_arrays(const pag_index_arrays* a, const std::vector<int>& devs) {
+    check_arrays(a);
+    auto ix = std::make_unique<pag_gpu_index>();
+    ix->n = a->n;
+    ix->dim = a->dim;
+    ix->padded = a->padded_dim;
+    ix->L = a->L;
+    ix->m = a->m;
+    ix->M = a->M;
+    ix->efC = a->efC;
+    ix->b_build = a->b_build;
+    ix->pes_flush = a->pes_flush_interval;
+    ix->seed = a->seed;
+    ix->metric = a->metric;
+    ix->enable_pes = a->enable_pes;
+    ix->entries.assign(a->entry_nodes, a->entry_nodes + a->n_entries);
+    init_layout(*ix);
+    const uint64_t n = ix->n;
+    const uint32_t S = ix->slot_stride, cb = ix->cb, cwp = ix->cwp, maxdeg = ix->maxdeg;
+    IndexSource src;
+    src.node = [&](uint64_t u, uint8_t* blk) {
+        const uint32_t deg = a->degrees[u];
+        if (deg > maxdeg) throw_err(PAG_GPU_ERUNTIME, "degree over cap in file");
+        fill_block_arrays(blk, *a, u, deg, n, S, cb, cwp);
+        return deg;
+    };
+    src.rows = [&] { return reinterpret_cast<const uint8_t*>(a->rows); };
+    src.norms = [&] { return reinterpret_cast<const uint8_t*>(a->norms); };
+    upload_index(ix.get(), devs, false, src);
+    return ix;
+}
+
+void refresh_arrays(pag_gpu_index& ix, const pag_index_arrays* a, uint64_t* st) {
+    check_arrays(a);
+    RefreshSource src;
+    src.n_new = a->n;
+    src.dim = a->dim;
+    src.padded = a->padded_dim;
+    src.L = a->L;
+    src.m = a->m;
+    src.M = a->M;
+    src.seed = a->seed;
+    src.metric = a->metric;
+    src.entries = a->entry_nodes;
+    src.n_entries = a->n_entries;
+    const uint64_t n_new = a->n;
+    const uint32_t S = ix.slot_stride, cb = ix.cb, cwp = ix.cwp;
+    src.degree = [&](uint64_t u) { return a->degrees[u]; };
+    src.fill = [&](uint64_t u, uint32_t deg, uint8_t* blk) { fill_block_arrays(blk, *a, u, deg, n_new, S, cb, cwp); };
+    src.rows = reinterpret_cast<const uint8_t*>(a->rows);
+    src.norms = reinterpret_cast<const uint8_t*>(a->norms);
+    refresh_from(ix, src, st);
 }
 
 template <typename F>
@@ -1659,6 +1847,28 @@ int pag_gpu_open_devices(const char* index_path, const int* devices, uint32_t n_
         std::vector<int> devs(devices, devices + n_devices);
         if (devs.empty()) devs.push_back(0);
         *out = open_checked(index_path, devs).release();
+    });
+}
+
+int pag_gpu_open_from_arrays(const pag_index_arrays* a, const int* devices, uint32_t n_devices,
+                             pag_gpu_index** out) {
+    return guarded([&] {
+        if (!out || (n_devices && !devices)) throw_err(PAG_GPU_EINVAL, "null argument");
+        *out = nullptr;
+        std::vector<int> devs(devices, devices + n_devices);
+        if (devs.empty()) devs.push_back(0);
+        auto ix = open_arrays(a, devs);
+        update_dup_nodes(*ix);
+        *out = ix.release();
+    });
+}
+
+int pag_gpu_refresh_from_arrays(pag_gpu_index* ix, const pag_index_arrays* a, uint64_t* stats) {
+    return guarded([&] {
+        if (!ix) throw_err(PAG_GPU_EINVAL, "null argument");
+        std::lock_guard<std::mutex> g(ix->mu);
+        refresh_arrays(*ix, a, stats);
+        update_dup_nodes(*ix);
     });
 }
 

@@ -20,7 +20,7 @@ from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
-from ._lib import SearchParamsC, SearchStatsC, check, lib
+from ._lib import IndexArraysC, SearchParamsC, SearchStatsC, check, lib
 from .recall import mean_recall, recall_at_k  # noqa: F401  (bench.hpp:22-24, re-exported)
 
 Candidate = Tuple[int, float]  # (id, squared distance), builder.hpp:18-21
@@ -118,18 +118,109 @@ class ConstructionResult(BatchResult):
         return [int(x) for x in self.pes[i, :int(self.pes_n[i])]]
 
 
+@dataclass
+class IndexArrays:
+    """The reference's in-memory PagIndex as host arrays (builder.hpp:62-132):
+    the header parameters, and the fixed-stride storage the accessors
+    targets(u) / scalars(u) / edge_codes(u, j) / vectors().row(i) expose.
+    The source of PagIndex.from_arrays / refresh_from_arrays."""
+    dim: int
+    padded_dim: int
+    L: int
+    m: int
+    M: int
+    efC: int
+    b_build: int
+    pes_flush_interval: int
+    seed: int
+    metric: int            # 0 euclidean, 1 cosine
+    enable_pes: bool
+    entry_nodes: np.ndarray  # u32
+    degrees: np.ndarray      # n u32
+    targets: np.ndarray      # n x 2M u32
+    scalars: np.ndarray      # n x 2M x 3 f32 {cos_beta, edge_norm, base_offset}
+    codes: np.ndarray        # n x 2M x ceil(L/2) u8
+    rows: np.ndarray         # n x padded_dim f32
+    norms: Optional[np.ndarray] = None  # n f32 (None: computed from the rows)
+
+    @property
+    def n(self) -> int:
+        return int(self.degrees.shape[0])
+
+    @classmethod
+    def from_file(cls, path: str) -> "IndexArrays":
+        """load_index (builder.cpp:434-492) into host arrays: the PAGIDX01 v1
+        records restored into the fixed-stride layout (restore_edge)."""
+        buf = np.fromfile(path, np.uint8)
+        hdr = np.frombuffer(buf[:66].tobytes(), np.dtype([
+            ("magic", "<u8"), ("version", "<u4"), ("n", "<u8"), ("dim", "<u4"), ("padded", "<u4"), ("L", "<u4"),
+            ("m", "<u4"), ("M", "<u4"), ("efC", "<u4"), ("b_build", "<u4"), ("pes", "<u4"), ("seed", "<u8"),
+            ("metric", "u1"), ("enable_pes", "u1"), ("n_entries", "<u4")]))[0]
+        if int(hdr["magic"]) != 0x5041474944583031:
+            raise RuntimeError("bad index magic")
+        if int(hdr["version"]) != 1:
+            raise RuntimeError("unsupported index version")
+        n, padded, M = int(hdr["n"]), int(hdr["padded"]), int(hdr["M"])
+        L = int(hdr["L"]) or int(lib.pag_gpu_default_subspace_count(int(hdr["dim"])))
+        cb, cap, ne = (L + 1) // 2, 2 * M, int(hdr["n_entries"])
+        off = 66
+        entries = np.frombuffer(buf[off:off + 4 * ne].tobytes(), "<u4").copy()
+        off += 4 * ne
+        deg = np.zeros(n, np.uint32)
+        tg = np.zeros((n, cap), np.uint32)
+        sc = np.zeros((n, cap, 3), np.float32)
+        cd = np.zeros((n, cap, cb), np.uint8)
+        rec = np.dtype([("t", "<u4"), ("codes", "u1", (cb,)), ("sc", "<f4", (3,))])
+        for u in range(n):
+            d = int(np.frombuffer(buf[off:off + 4].tobytes(), "<u4")[0])
+            off += 4
+            if d > cap:
+                raise RuntimeError("degree over cap in file")
+            r = np.frombuffer(buf[off:off + rec.itemsize * d].tobytes(), rec)
+            off += rec.itemsize * d
+            deg[u], tg[u, :d], cd[u, :d], sc[u, :d] = d, r["t"], r["codes"], r["sc"]
+        rows = np.frombuffer(buf[off:off + 4 * n * padded].tobytes(), "<f4").reshape(n, padded).copy()
+        off += 4 * n * padded
+        norms = np.frombuffer(buf[off:off + 4 * n].tobytes(), "<f4").copy()
+        if norms.shape[0] != n:
+            raise RuntimeError("index read failed")
+        return cls(int(hdr["dim"]), padded, L, int(hdr["m"]), M, int(hdr["efC"]), int(hdr["b_build"]),
+                   int(hdr["pes"]), int(hdr["seed"]), int(hdr["metric"]), bool(hdr["enable_pes"]), entries, deg, tg,
+                   sc, cd, rows, norms)
+
+    def to_c(self):
+        """(pag_index_arrays, the contiguous arrays it borrows)."""
+        keep = [np.ascontiguousarray(self.entry_nodes, np.uint32), np.ascontiguousarray(self.degrees, np.uint32),
+                np.ascontiguousarray(self.targets, np.uint32), np.ascontiguousarray(self.scalars, np.float32),
+                np.ascontiguousarray(self.codes, np.uint8), np.ascontiguousarray(self.rows, np.float32),
+                None if self.norms is None else np.ascontiguousarray(self.norms, np.float32)]
+        a = IndexArraysC()
+        a.n, a.dim, a.padded_dim, a.L, a.m, a.M = self.n, self.dim, self.padded_dim, self.L, self.m, self.M
+        a.efC, a.b_build, a.pes_flush_interval, a.seed = self.efC, self.b_build, self.pes_flush_interval, self.seed
+        a.metric, a.enable_pes, a.n_entries = self.metric, int(self.enable_pes), keep[0].shape[0]
+        (a.entry_nodes, a.degrees, a.targets, a.scalars, a.codes, a.rows, a.norms) = (
+            None if k is None else k.ctypes.data for k in keep)
+        return a, keep
+
+
 class PagIndex:
     """A PAGIDX01 index resident in HBM on one or more GPUs (move-only in the
     reference, builder.hpp:62-69; here a handle released by close())."""
 
-    def __init__(self, path: str, devices: Sequence[int] = (0,)):
+    def __init__(self, path: Optional[str], devices: Sequence[int] = (0,), arrays: Optional[IndexArrays] = None):
         """One replica per entry of `devices` (CUDA device ordinals; an entry
         may repeat, giving several replicas on one GPU). Batches are split
-        into contiguous shards, one per replica (pag_gpu_open_devices)."""
+        into contiguous shards, one per replica (pag_gpu_open_devices).
+        With `arrays` the source is the in-memory index (pag_gpu_open_from_arrays)."""
         devs = [int(d) for d in devices] or [0]
         arr = (C.c_int * len(devs))(*devs)
         self._h = C.c_void_p()
-        check(lib.pag_gpu_open_devices(path.encode(), arr, len(devs), C.byref(self._h)))
+        if arrays is not None:
+            a, keep = arrays.to_c()
+            check(lib.pag_gpu_open_from_arrays(C.byref(a), arr, len(devs), C.byref(self._h)))
+            del keep
+        else:
+            check(lib.pag_gpu_open_devices(path.encode(), arr, len(devs), C.byref(self._h)))
         info = np.zeros(16, np.uint64)
         check(lib.pag_gpu_info(self._h, info, 16))
         (self.n, self.dim, self.padded_dim, self.L, self.m, self.M, metric, self.n_entries,
@@ -318,6 +409,23 @@ class PagIndex:
         check(lib.pag_gpu_info(self._h, info, 12))
         self.n, self.total_edges, self.device_bytes = int(info[0]), int(info[9]), int(info[11])
         self.path = path
+        return {"new_nodes": int(st[0]), "changed_blocks": int(st[1]), "bytes_uploaded": int(st[2]),
+                "seconds": int(st[3]) / 1e6}
+
+    @classmethod
+    def from_arrays(cls, arrays: IndexArrays, devices: Sequence[int] = (0,)) -> "PagIndex":
+        """The in-memory index as the source (no file round trip)."""
+        return cls(None, devices, arrays=arrays)
+
+    def refresh_from_arrays(self, arrays: IndexArrays) -> dict:
+        """refresh() with the in-memory index as the newer state."""
+        st = np.zeros(4, np.uint64)
+        a, keep = arrays.to_c()
+        check(lib.pag_gpu_refresh_from_arrays(self._h, C.byref(a), st))
+        del keep
+        info = np.zeros(12, np.uint64)
+        check(lib.pag_gpu_info(self._h, info, 12))
+        self.n, self.total_edges, self.device_bytes = int(info[0]), int(info[9]), int(info[11])
         return {"new_nodes": int(st[0]), "changed_blocks": int(st[1]), "bytes_uploaded": int(st[2]),
                 "seconds": int(st[3]) / 1e6}
 

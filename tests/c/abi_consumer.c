@@ -18,6 +18,11 @@ _Static_assert(offsetof(pag_search_stats, edges_scanned) == 32, "edges_scanned o
 _Static_assert(sizeof(pag_search_params) == 16, "pag_search_params: three u32 + four u8");
 _Static_assert(offsetof(pag_search_params, use_prt) == 12, "use_prt offset");
 _Static_assert(offsetof(pag_search_params, exact_dist) == 14, "exact_dist offset");
+_Static_assert(sizeof(pag_index_arrays) == 112, "pag_index_arrays: u64, 8 x u32, u64, 4 x u8, u32, 7 pointers");
+_Static_assert(offsetof(pag_index_arrays, seed) == 40, "seed offset");
+_Static_assert(offsetof(pag_index_arrays, n_entries) == 52, "n_entries offset");
+_Static_assert(offsetof(pag_index_arrays, entry_nodes) == 56, "entry_nodes offset");
+_Static_assert(offsetof(pag_index_arrays, norms) == 104, "norms offset");
 
 #define CHECK(c)                                                       \
     do {                                                               \
@@ -53,6 +58,16 @@ int main(int argc, char** argv) {
     CHECK(info[0] > 0 && info[1] > 0 && info[2] >= info[1] && info[9] > 0);
     rc = pag_gpu_inspect("/nonexistent/pag.bin", info, 12);
     CHECK(rc == PAG_GPU_ERUNTIME && strcmp(pag_gpu_last_error(), "cannot open index: /nonexistent/pag.bin") == 0);
+    {   /* the in-memory source: argument errors are raised before any GPU work */
+        pag_index_arrays a;
+        pag_gpu_index* h = NULL;
+        memset(&a, 0, sizeof a);
+        CHECK(pag_gpu_open_from_arrays(NULL, NULL, 0, &h) == PAG_GPU_EINVAL && h == NULL);
+        a.n = 4; /* n > 0 with no arrays */
+        CHECK(pag_gpu_open_from_arrays(&a, NULL, 0, &h) == PAG_GPU_EINVAL && h == NULL);
+        CHECK(strcmp(pag_gpu_last_error(), "null argument") == 0);
+        CHECK(pag_gpu_refresh_from_arrays(NULL, &a, NULL) == PAG_GPU_EINVAL);
+    }
     CHECK(strstr(pag_gpu_version(), "sm_100a") != NULL);
     printf("ok n=%llu dim=%llu padded=%llu edges=%llu\n", (unsigned long long)info[0], (unsigned long long)info[1],
            (unsigned long long)info[2], (unsigned long long)info[9]);

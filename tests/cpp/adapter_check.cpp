@@ -5,11 +5,16 @@
 // queries, that pag::search_batch on the GPU equals the reference library's
 // pag::search (proj/src/routing.cpp:249-261) bit for bit, that the
 // construction search equals search_padded with the build parameters
-// (builder.cpp:218-227), and that errors surface as the reference's
-// exception classes. Built by tests/cpp/Makefile into oracle/_ref/ (it
+// (builder.cpp:218-227), that a GpuIndex opened straight from the in-memory
+// PagIndex (pag_gpu_open_from_arrays) searches like the one opened from the
+// file, that after insert_online batches on the PagIndex a refresh from
+// memory (pag_gpu_refresh_from_arrays) makes the GPU search equal the
+// reference's search of the extended index, and that errors surface as the
+// reference's exception classes. Built by tests/cpp/Makefile into oracle/_ref/ (it
 // links the reference objects compiled from /root/reference/proj/src).
 //
 // usage: adapter_check <index.pagidx> <queries.fvecs> <K> <efS>
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -79,6 +84,33 @@ int main(int argc, char** argv) {
     size_t c_equal = 0;
     for (size_t i = 0; i < nodes.size(); ++i)
         c_equal += same(cons[i], pag::search_padded(ref, ref.vectors().row(nodes[i]), bp, state), true);
+    // the in-memory PagIndex as the source: same results as the file-based handle
+    pag::PagIndex live = pag::load_index(argv[1]);
+    pag::GpuIndex mem(live);
+    const auto got_mem = pag::search_batch(mem, qs, sp);
+    size_t a_equal = 0;
+    for (size_t i = 0; i < nq; ++i) a_equal += same(got_mem[i], got[i], false);
+    // online inserts on the PagIndex (builder.cpp:354-363), two batches, then a
+    // refresh from memory; the GPU must search the extended index like the reference
+    size_t r_equal = 0, r_total = 0;
+    {
+        pag::PesSet pes;
+        const size_t per_batch = std::min<size_t>(nq / 2, 12);
+        size_t next = 0;
+        for (int batch = 0; batch < 2; ++batch) {
+            for (size_t i = 0; i < per_batch; ++i, ++next) {
+                std::vector<float> x(qs.begin() + next * d, qs.begin() + (next + 1) * d);
+                for (auto& v : x) v = v * 0.75f + 0.01f * static_cast<float>(i + 1);  // not a duplicate of a query
+                pag::insert_online(live, x, pes);
+            }
+            mem.refresh(live);
+            const auto after = pag::search_batch(mem, qs, sp);
+            for (size_t i = 0; i < nq; ++i, ++r_total)
+                r_equal += same(after[i], pag::search(live, std::span<const float>(qs.data() + i * d, d), sp, state),
+                                false);
+        }
+        if (mem.size() != live.size()) r_equal = 0;
+    }
     // errors: the reference's exception classes and texts
     bool err_ok = false;
     try {
@@ -95,7 +127,11 @@ int main(int argc, char** argv) {
         open_ok = std::string(e.what()).find("cannot open index") == 0;
     }
     std::printf("{\"queries\": %zu, \"queries_equal\": %zu, \"nodes\": %zu, \"nodes_equal\": %zu, "
+                "\"from_arrays_equal\": %zu, \"after_refresh\": %zu, \"after_refresh_equal\": %zu, "
                 "\"k_gt_efs_invalid_argument\": %s, \"open_runtime_error\": %s}\n",
-                nq, q_equal, nodes.size(), c_equal, err_ok ? "true" : "false", open_ok ? "true" : "false");
-    return (q_equal == nq && c_equal == nodes.size() && err_ok && open_ok) ? 0 : 1;
+                nq, q_equal, nodes.size(), c_equal, a_equal, r_total, r_equal, err_ok ? "true" : "false",
+                open_ok ? "true" : "false");
+    return (q_equal == nq && c_equal == nodes.size() && a_equal == nq && r_equal == r_total && err_ok && open_ok)
+               ? 0
+               : 1;
 }

@@ -6,8 +6,11 @@ and runs the host-only entry points; the C++ adapter include/pag_gpu.hpp
 (the reference-side binding of INTEGRATION.md §2) compiles and links against
 the reference's own headers and library (tests/cpp/adapter_check.cpp).
 GPU: that C++ program checks, in one process, pag::search_batch on the GPU
-against the reference library's pag::search, and the construction search
-against search_padded, bit for bit, plus the exception mapping."""
+against the reference library's pag::search, the construction search
+against search_padded, a handle opened from the in-memory PagIndex
+(pag_gpu_open_from_arrays) and refreshed from memory after insert_online
+batches (pag_gpu_refresh_from_arrays), bit for bit, plus the exception
+mapping."""
 from __future__ import annotations
 
 import json
@@ -49,4 +52,7 @@ def test_cpp_adapter_equals_reference_in_process(built, name, K, efS):
     assert out.returncode == 0, out.stdout + out.stderr
     r = json.loads(out.stdout.strip().splitlines()[-1])
     assert r["queries_equal"] == r["queries"] and r["nodes_equal"] == r["nodes"]
+    # opened from the in-memory PagIndex; refreshed from memory after insert_online batches
+    assert r["from_arrays_equal"] == r["queries"]
+    assert r["after_refresh"] == 2 * r["queries"] and r["after_refresh_equal"] == r["after_refresh"]
     assert r["k_gt_efs_invalid_argument"] and r["open_runtime_error"]

@@ -62,3 +62,44 @@ def test_refresh_matches_oracle_each_phase(phases):
             ix.refresh(idx)  # shrinking is refused
     finally:
         ix.close()
+
+
+@pytest.mark.gpu
+def test_in_memory_source_equals_the_file_source(phases):
+    """pag_gpu_open_from_arrays / pag_gpu_refresh_from_arrays: the reference's
+    in-memory storage (IndexArrays, here restored from the phase files) as the
+    source; searches, construction searches and ground truth equal the
+    file-opened handle's and the oracle's, with and without cached norms."""
+    import paper_2603_06660_b200 as pag
+    idx, files, q = phases
+    a0 = pag.IndexArrays.from_file(idx)
+    mem = pag.PagIndex.from_arrays(a0)
+    a0.norms = None
+    mem2 = pag.PagIndex.from_arrays(a0, devices=(0, 0))  # norms recomputed; two replicas
+    dsk = pag.load_index(idx)
+    try:
+        assert (mem.n, mem.dim, mem.L, mem.efC, mem.total_edges) == (dsk.n, dsk.dim, dsk.L, dsk.efC, dsk.total_edges)
+        for path in [None] + files:
+            if path is not None:
+                st = mem.refresh_from_arrays(pag.IndexArrays.from_file(path))
+                st2 = dsk.refresh(path)
+                assert (st["new_nodes"], st["changed_blocks"]) == (st2["new_nodes"], st2["changed_blocks"])
+                a = pag.IndexArrays.from_file(path)
+                a.norms = None
+                mem2.refresh_from_arrays(a)
+            want = O.OracleIndex(path or idx).search(q, 10, 60)
+            for ix in (mem, mem2, dsk):
+                got = ix.search_batch(q, pag.SearchParams(K=10, efS=60))
+                assert_same_results((got.ids, got.sq, got.n_out, got.stats), want, str(path))
+            gi, gs = dsk.ground_truth(q, 10)
+            for ix in (mem, mem2):
+                mi, ms = ix.ground_truth(q, 10)
+                assert np.array_equal(mi, gi) and np.array_equal(ms.view(np.uint32), gs.view(np.uint32))
+            nodes = np.arange(0, dsk.n, 37, dtype=np.uint32)
+            c0, c1 = dsk.construction_search(nodes), mem.construction_search(nodes)
+            assert np.array_equal(c0.ids, c1.ids) and np.array_equal(c0.pes_n, c1.pes_n)
+        with pytest.raises(ValueError, match="not an extension"):
+            mem.refresh_from_arrays(pag.IndexArrays.from_file(idx))
+    finally:
+        for ix in (mem, mem2, dsk):
+            ix.close()
