@@ -1105,8 +1105,10 @@ CUtensorMap tensor_map_rows(const float* base, uint64_t rows, uint32_t padded, u
     return m;
 }
 
-// bench.cpp:18-53. k <= 32: tensor-core candidates + exact re-rank +
-// certificate (uncertified queries re-run exactly); otherwise exact SIMT.
+// bench.cpp:18-53. k <= 1000: tensor-core filter GEMM under a per-query bound
+// + exact re-rank of the pool (or, on request, per-split candidate lists +
+// certificate for k <= 32); queries not settled that way re-run exactly;
+// k > 1000: exact SIMT.
 // Returns the number of queries whose tensor-core candidates were not
 // certified and were re-run exactly.
 uint64_t ground_truth_on_replica(pag_gpu_index& ix, Replica& r, const float* q, uint64_t nq, uint32_t k,
@@ -1120,17 +1122,21 @@ uint64_t ground_truth_on_replica(pag_gpu_index& ix, Replica& r, const float* q, 
     DevBuf d_q(4 * qp.size()), d_ids(4ull * nq * kk), d_sq(4ull * nq * kk);
     cuda_check(cudaMemcpy(d_q.p, qp.data(), 4 * qp.size(), cudaMemcpyHostToDevice), "H2D");
     const bool no_tc = !r.bnorm || std::getenv("PAG_GPU_GT_EXACT");
-    // k <= 32: per-split top-C lists; 32 < k <= 1000 (or PAG_GPU_GT_POOL set):
-    // per-query bound + pool; otherwise the exact SIMT kernel
-    const bool pool = !no_tc && kk <= 1000 && (kk > pagdev::gt_tc_cmax() / 2 || std::getenv("PAG_GPU_GT_POOL"));
-    const bool tc = !no_tc && !pool && kk <= pagdev::gt_tc_cmax() / 2;
+    // k <= 1000: per-query bound + pool (a graph search supplies the bound
+    // rows); PAG_GPU_GT_LISTS: the per-split top-C lists for k <= 32 (needs no
+    // search; cfg-2 k = 10: 0.154 s against the pool path's time in
+    // profiles/); otherwise the exact SIMT kernel
+    const bool lists = !no_tc && kk <= pagdev::gt_tc_cmax() / 2 && std::getenv("PAG_GPU_GT_LISTS");
+    const bool pool = !no_tc && !lists && kk <= 1000;
+    const bool tc = lists;
     std::vector<uint32_t> redo;
     if (pool) {
         // 1. k rows per query from a graph search of the raw query (ids only;
         //    any k distinct rows give the bound)
         pag_search_params sp;
         pag_gpu_default_params(&sp);
-        sp.K = sp.efS = kk;
+        sp.K = kk;
+        sp.efS = std::max(kk, 64u);  // a few more expansions tighten the bound of a small k
         sp.exact_dist = 0;
         DevBuf rawq(4ull * nq * ix.dim), sids(4ull * nq * kk), ssq(4ull * nq * kk), sn(4ull * nq),
             sst(4ull * nq * pagdev::kStatWords);

@@ -146,20 +146,21 @@ def test_ground_truth_bitexact(pag, built, name, k):
                                          ("tail10", 16, False), ("cos20", 8, False), ("deg64", 25, False),
                                          ("euc48", 100, False), ("deg64", 1000, False), ("pad30", 200, False),
                                          ("cos20", 64, False), ("unit512", 1000, False), ("euc48", 10, True),
-                                         ("pad9c", 5, True)])
+                                         ("pad9c", 5, True), ("euc48", 1, True), ("cos20", 8, True),
+                                         ("tail10", 16, True), ("deg64", 25, True)])
 def test_tensor_core_ground_truth_equals_exact(pag, built, monkeypatch, name, k, pool):
     """tcgen05 TF32 GEMM ground truth gives the same ids and bits as the exact
-    SIMT kernel and the oracle, with every query certified: k <= 32 by
-    per-split top-C candidates + certificate, 32 < k <= 1000 (and, forced,
-    small k) by the per-query bound + pool path."""
+    SIMT kernel and the oracle, with every query certified: by the per-query
+    bound + pool path (the default for k <= 1000), and for k <= 32 also by the
+    per-split top-C candidate lists + certificate (pool = False rows)."""
     fx = built(name)
     ix = gpu_index(pag, fx["index"])
-    if pool:
-        monkeypatch.setenv("PAG_GPU_GT_POOL", "1")
+    if not pool and k <= 32:
+        monkeypatch.setenv("PAG_GPU_GT_LISTS", "1")
     before = ix.gt_uncertified()
     ti, ts = ix.ground_truth(fx["queries"], k)
     assert ix.gt_uncertified() == before, "tensor-core candidates not certified"
-    monkeypatch.delenv("PAG_GPU_GT_POOL", raising=False)
+    monkeypatch.delenv("PAG_GPU_GT_LISTS", raising=False)
     monkeypatch.setenv("PAG_GPU_GT_EXACT", "1")
     ei, es = ix.ground_truth(fx["queries"], k)
     assert np.array_equal(ti, ei) and np.array_equal(ts.view(np.uint32), es.view(np.uint32))
