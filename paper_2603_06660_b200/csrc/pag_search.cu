@@ -65,6 +65,11 @@ __device__ unsigned long long g_phase[8];
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint32_t EMPTY = 0xffffffffu;
 constexpr uint32_t VISITED = 0x80000000u;
+#ifdef PAG_VALIDATE
+constexpr bool kRingsAlways = true;   // validate_state inspects the rings
+#else
+constexpr bool kRingsAlways = false;
+#endif
 
 __device__ __forceinline__ bool cless(float sa, uint32_t ia, float sb, uint32_t ib) {
     return sa < sb || (sa == sb && ia < ib);  // candidate_less, builder.hpp:23-25
@@ -446,6 +451,11 @@ __device__ __noinline__ Arr warp_sort(Arr a, Arr t, uint32_t n, int lane) {
 // ---------------------------------------------------------------------------
 struct TfbReg {
     uint32_t b;
+    // a single-round search (r_max == 1) never reads its rings: end_round is
+    // not reached (routing.cpp:238-242: break before it after the last
+    // round) and ring contents never reach the results, so ring pushes are
+    // skipped there (kept in PAG_VALIDATE builds, which inspect the rings)
+    bool rings_live;
     uint32_t w_id, w_deg;
     float w_sq;
     bool w_vis;
@@ -459,6 +469,7 @@ struct TfbReg {
 
     __device__ void init(uint32_t b_, uint8_t* sw, uint8_t* gw, const SearchLaunch& P) {
         b = b_;
+        rings_live = kRingsAlways || P.r_max > 1;
         rf_base = (P.rings_in_smem ? sw : gw) + P.off_rf;
     }
     __device__ void reset() {
@@ -575,10 +586,12 @@ struct TfbReg {
             return;
         }
         const uint32_t z = zmax_idx;
-        const uint32_t oid = __shfl_sync(FULL, w_id, z);
-        const float osq = __shfl_sync(FULL, w_sq, z);
-        const uint32_t odeg = __shfl_sync(FULL, w_deg, z);
-        push_rt(oid, osq, odeg, lane);
+        if (rings_live) {
+            const uint32_t oid = __shfl_sync(FULL, w_id, z);
+            const float osq = __shfl_sync(FULL, w_sq, z);
+            const uint32_t odeg = __shfl_sync(FULL, w_deg, z);
+            push_rt(oid, osq, odeg, lane);
+        }
         if (static_cast<uint32_t>(lane) == z) {
             w_id = id;
             w_sq = sq;
@@ -700,6 +713,7 @@ template <bool WOFF>
 struct TfbMemT {
     Arr W, rf, rt, mi;
     uint32_t b, S;
+    bool rings_live;  // (see TfbReg)
     uint32_t wsize, rf_head, rf_size, rt_head, rt_size;
     float zmax_sq, zmax_dist;
     uint32_t zmax_idx;
@@ -717,6 +731,7 @@ struct TfbMemT {
     __device__ void init(uint32_t b_, uint8_t* sw, uint8_t* gw, const SearchLaunch& P) {
         b = b_;
         S = (b + 31) / 32;
+        rings_live = kRingsAlways || P.r_max > 1;
         W = make_arr((P.W_in_smem ? sw : gw) + P.off_W, b);
         rf = make_arr((P.rings_in_smem ? sw : gw) + P.off_rf, b);
         rt = make_arr((P.rings_in_smem ? sw : gw) + P.off_rt, b);
@@ -980,7 +995,9 @@ struct TfbMemT {
             return;
         }
         const uint32_t z = zmax_idx;
-        if (WOFF) {
+        if (!rings_live) {
+            // single round: R_T is never read
+        } else if (WOFF) {
             ring_push(rt, b, rt_head, rt_size, zmax_id, zmax_sq, zmax_aux & ~VISITED, lane);
         } else {
             const uint32_t oid = W.id[z];
@@ -1539,7 +1556,7 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
                 rem &= pm;
                 const uint32_t am = __ballot_sync(FULL, pl && sqv < asq);
                 const uint32_t fp = pm & (am ? (am & (0u - am)) - 1u : 0xffffffffu);
-                if (fp) s.push_fp_many(fp, w, sqv, dgv, lane);
+                if (fp && s.rings_live) s.push_fp_many(fp, w, sqv, dgv, lane);
                 passed |= fp;
                 if (!am) break;
                 const int k = __ffs(am) - 1;
@@ -1588,7 +1605,7 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
             if (sq_j < s.admission_sq()) {
                 s.admit(w_j, sq_j, deg_j, lane);
             } else {
-                s.push_fp(w_j, sq_j, deg_j, lane);
+                if (s.rings_live) s.push_fp(w_j, sq_j, deg_j, lane);
             }
         }
         // marks of this group's passes (routing.cpp:183). Later lookups come

@@ -19,13 +19,13 @@ P="python bench.py --efs 70 --steps 4 --warmup 3 --no-cpu-baseline --no-e2e"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --print-units base --log-file $R/launches_cfg2.csv $P > $R/ncu_launches.log 2>&1; echo ncu_l=$?
 for d in warp-tree exact; do
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv --print-units base -k regex:pag_search -s 3 -c 1 $P --dist $d > $R/traffic_cfg2_$d.csv 2> $R/traffic_cfg2_$d.err; echo ncu_t$d=$?
-  ncu --set full --clock-control none --import-source on -k regex:pag_search -s 3 -c 1 -o $R/full_cfg2_$d $P --dist $d > $R/ncu_full_cfg2_$d.log 2>&1; echo ncu_f$d=$?
-  python tools/ncu_summary.py $R/full_cfg2_$d.ncu-rep 30 > $R/full_cfg2_$d.txt 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:pag_search -s 3 -c 1 -o /tmp/full_cfg2_$d $P --dist $d > $R/ncu_full_cfg2_$d.log 2>&1; echo ncu_f$d=$?
+  python tools/ncu_summary.py /tmp/full_cfg2_$d.ncu-rep 30 > $R/full_cfg2_$d.txt 2>&1
 done
 C="python bench.py --mode construction --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv --print-units base -k regex:pag_search -s 3 -c 1 $C > $R/traffic_cons.csv 2> $R/traffic_cons.err; echo ncu_tc=$?
-ncu --set full --clock-control none --import-source on -k regex:pag_search -s 3 -c 1 -o $R/full_cons $C > $R/ncu_full_cons.log 2>&1; echo ncu_fc=$?
-python tools/ncu_summary.py $R/full_cons.ncu-rep 30 > $R/full_cons.txt 2>&1
+ncu --set full --clock-control none --import-source on -k regex:pag_search -s 3 -c 1 -o /tmp/full_cons $C > $R/ncu_full_cons.log 2>&1; echo ncu_fc=$?
+python tools/ncu_summary.py /tmp/full_cons.ncu-rep 30 > $R/full_cons.txt 2>&1
 G="python tools/gt_tc_bench.py cfg2 1000"
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,sm__inst_executed_pipe_uma.sum --clock-control none --csv --print-units base -k regex:gt_tc -c 12 $G > $R/ncu_gt_cfg2.csv 2> $R/ncu_gt_cfg2.err; echo ncu_gt=$?
 for f in $R/bench_*.json; do echo $f; python -c "import json; d=json.load(open('$f')); print(d.get('value'), (d.get('roofline') or {}).get('frac'), (d.get('e2e') or {}).get('value'), (d.get('cpu_baseline') or {}).get('value'))"; done
@@ -37,8 +37,8 @@ for c in cfg3 cfg4; do
   echo "$c efS=$E nq=$N" > $R/op_$c.txt
   P="python bench.py --config $c --efs $E --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv --print-units base -k regex:pag_search -s 3 -c 1 $P > $R/traffic_$c.csv 2> $R/traffic_$c.err; echo ncu_t$c=$?
-  ncu --set full --clock-control none --import-source on -k regex:pag_search -s 3 -c 1 -o $R/full_$c $P > $R/ncu_full_$c.log 2>&1; echo ncu_f$c=$?
-  python tools/ncu_summary.py $R/full_$c.ncu-rep 30 > $R/full_$c.txt 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:pag_search -s 3 -c 1 -o /tmp/full_$c $P > $R/ncu_full_$c.log 2>&1; echo ncu_f$c=$?
+  python tools/ncu_summary.py /tmp/full_$c.ncu-rep 30 > $R/full_$c.txt 2>&1
 done
 timeout 900 python tools/gt_tc_bench.py cfg3 100 > $R/gt_cfg3.jsonl 2> $R/gt_cfg3.err; echo gt3=$?
 timeout 900 python tools/gt_tc_bench.py cfg4 1000 > $R/gt_cfg4.jsonl 2> $R/gt_cfg4.err; echo gt4=$?
