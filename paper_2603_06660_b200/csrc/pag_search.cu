@@ -65,11 +65,19 @@ __device__ unsigned long long g_phase[8];
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint32_t EMPTY = 0xffffffffu;
 constexpr uint32_t VISITED = 0x80000000u;
+// A single-round search (r_max == 1) never reads its rings: end_round is not
+// reached (routing.cpp:238-242 breaks before it after the last round) and
+// ring contents never reach the results, so ring pushes are skipped there
+// (kept in PAG_VALIDATE builds, whose validate_state inspects the rings).
+// Evaluated from the kernel parameter where used (no register held).
+__device__ __forceinline__ bool rings_are_read(const SearchLaunch& P) {
 #ifdef PAG_VALIDATE
-constexpr bool kRingsAlways = true;   // validate_state inspects the rings
+    (void)P;
+    return true;
 #else
-constexpr bool kRingsAlways = false;
+    return P.r_max > 1;
 #endif
+}
 
 __device__ __forceinline__ bool cless(float sa, uint32_t ia, float sb, uint32_t ib) {
     return sa < sb || (sa == sb && ia < ib);  // candidate_less, builder.hpp:23-25
@@ -451,11 +459,6 @@ __device__ __noinline__ Arr warp_sort(Arr a, Arr t, uint32_t n, int lane) {
 // ---------------------------------------------------------------------------
 struct TfbReg {
     uint32_t b;
-    // a single-round search (r_max == 1) never reads its rings: end_round is
-    // not reached (routing.cpp:238-242: break before it after the last
-    // round) and ring contents never reach the results, so ring pushes are
-    // skipped there (kept in PAG_VALIDATE builds, which inspect the rings)
-    bool rings_live;
     uint32_t w_id, w_deg;
     float w_sq;
     bool w_vis;
@@ -469,7 +472,6 @@ struct TfbReg {
 
     __device__ void init(uint32_t b_, uint8_t* sw, uint8_t* gw, const SearchLaunch& P) {
         b = b_;
-        rings_live = kRingsAlways || P.r_max > 1;
         rf_base = (P.rings_in_smem ? sw : gw) + P.off_rf;
     }
     __device__ void reset() {
@@ -579,8 +581,8 @@ struct TfbReg {
         }
         __syncwarp();
     }
-    // routing.cpp:55-69
-    __device__ void admit(uint32_t id, float sq, uint32_t deg, int lane) {
+    // routing.cpp:55-69 (rings_live: see rings_are_read)
+    __device__ void admit(uint32_t id, float sq, uint32_t deg, int lane, bool rings_live) {
         if (wsize < b) {
             append(id, sq, deg, lane);
             return;
@@ -713,7 +715,6 @@ template <bool WOFF>
 struct TfbMemT {
     Arr W, rf, rt, mi;
     uint32_t b, S;
-    bool rings_live;  // (see TfbReg)
     uint32_t wsize, rf_head, rf_size, rt_head, rt_size;
     float zmax_sq, zmax_dist;
     uint32_t zmax_idx;
@@ -731,7 +732,6 @@ struct TfbMemT {
     __device__ void init(uint32_t b_, uint8_t* sw, uint8_t* gw, const SearchLaunch& P) {
         b = b_;
         S = (b + 31) / 32;
-        rings_live = kRingsAlways || P.r_max > 1;
         W = make_arr((P.W_in_smem ? sw : gw) + P.off_W, b);
         rf = make_arr((P.rings_in_smem ? sw : gw) + P.off_rf, b);
         rt = make_arr((P.rings_in_smem ? sw : gw) + P.off_rt, b);
@@ -989,7 +989,7 @@ struct TfbMemT {
         }
         __syncwarp();
     }
-    __device__ void admit(uint32_t id, float sq, uint32_t deg, int lane) {
+    __device__ void admit(uint32_t id, float sq, uint32_t deg, int lane, bool rings_live) {
         if (wsize < b) {
             append(id, sq, deg, lane);
             return;
@@ -1556,7 +1556,7 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
                 rem &= pm;
                 const uint32_t am = __ballot_sync(FULL, pl && sqv < asq);
                 const uint32_t fp = pm & (am ? (am & (0u - am)) - 1u : 0xffffffffu);
-                if (fp && s.rings_live) s.push_fp_many(fp, w, sqv, dgv, lane);
+                if (fp && rings_are_read(P)) s.push_fp_many(fp, w, sqv, dgv, lane);
                 passed |= fp;
                 if (!am) break;
                 const int k = __ffs(am) - 1;
@@ -1565,7 +1565,8 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
                 // many admissions are evicted unexpanded: cfg3 -1.8%)
                 if (P.b <= 32 && lane == k)
                     prefetch_l2_bulk(ix.adj + static_cast<uint64_t>(w) * ix.block_bytes, ix.block_bytes);
-                s.admit(__shfl_sync(FULL, w, k), __shfl_sync(FULL, sqv, k), __shfl_sync(FULL, dgv, k), lane);
+                s.admit(__shfl_sync(FULL, w, k), __shfl_sync(FULL, sqv, k), __shfl_sync(FULL, dgv, k), lane,
+                        rings_are_read(P));
                 passed |= 1u << k;
                 rem &= ~((2u << k) - 1u);
             }
@@ -1603,9 +1604,9 @@ __device__ bool expand(const SearchLaunch& P, Common& c, TFB& s, uint32_t slot, 
             const float sq_j = c.sqbuf[jl];
             const uint32_t deg_j = c.degbuf()[jl];
             if (sq_j < s.admission_sq()) {
-                s.admit(w_j, sq_j, deg_j, lane);
+                s.admit(w_j, sq_j, deg_j, lane, rings_are_read(P));
             } else {
-                if (s.rings_live) s.push_fp(w_j, sq_j, deg_j, lane);
+                if (rings_are_read(P)) s.push_fp(w_j, sq_j, deg_j, lane);
             }
         }
         // marks of this group's passes (routing.cpp:183). Later lookups come

@@ -13,6 +13,7 @@ for d in 0,0 0,0,0,0; do timeout 900 python bench.py --shard abi --devices $d --
 timeout 900 python bench.py --config cfg1 --steps 20 --warmup 5 > $R/bench_cfg1.json 2> $R/bench_cfg1.err; echo cfg1=$?
 timeout 900 python bench.py --mode construction --steps 5 --warmup 3 > $R/bench_cons.json 2> $R/bench_cons.err; echo cons=$?
 timeout 900 python tools/gt_tc_bench.py cfg2 10 100 1000 > $R/gt_cfg2.jsonl 2> $R/gt_cfg2.err; echo gt=$?
+timeout 900 python tools/gt_tc_bench.py cfg2 10 --lists > $R/gt_cfg2_lists.jsonl 2> $R/gt_cfg2_lists.err; echo gtl=$?
 timeout 900 python tools/recall_curve.py cfg2 10 20 40 60 70 80 100 150 200 300 400 > $R/recall_qps_cfg2.json 2> $R/curve_cfg2.err; echo curve=$?
 # ncu: launch list of the default bench command (timed steps), DRAM bytes per launch, one full capture per mode
 P="python bench.py --efs 70 --steps 4 --warmup 3 --no-cpu-baseline --no-e2e"
