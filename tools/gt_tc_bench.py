@@ -36,8 +36,7 @@ for k in ks:
     t2 = time.time() - t
     flop = 2.0 * len(q) * ix.n * ix.padded_dim
     print(json.dumps({"config": cfg_name, "k": k, "nq": len(q), "n": ix.n, "d": ix.padded_dim,
-                      "path": ("tc-lists" if (k <= 32 and os.environ.get("PAG_GPU_GT_LISTS")) else "tc-pool")
-                      if k <= 1000 else "exact",
+                      "path": ("tc-lists" if (k <= 32 and lists) else "tc-pool") if k <= 1000 else "exact",
                       "tc_s": round(t1, 4), "exact_s": round(t2, 4), "speedup": round(t2 / t1, 2),
                       "tc_gemm_equiv_tflops": round(flop / t1 / 1e12, 1),
                       "identical": bool(np.array_equal(gi, ei) and np.array_equal(gs.view(np.uint32),
