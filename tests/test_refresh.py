@@ -103,3 +103,27 @@ def test_in_memory_source_equals_the_file_source(phases):
     finally:
         for ix in (mem, mem2, dsk):
             ix.close()
+
+
+@pytest.mark.gpu
+def test_in_memory_source_is_validated_like_a_file(phases):
+    """load_index's checks (builder.cpp:434-492) hold for the in-memory source
+    too: a degree over the cap, an edge target past n and a padded_dim that
+    does not match L are refused with the file path's texts."""
+    import paper_2603_06660_b200 as pag
+    idx, _, _ = phases
+    a = pag.IndexArrays.from_file(idx)
+    bad = pag.IndexArrays(**{**a.__dict__, "degrees": a.degrees.copy()})
+    bad.degrees[7] = 2 * a.M + 1
+    with pytest.raises(RuntimeError, match="degree over cap"):
+        pag.PagIndex.from_arrays(bad)
+    bad = pag.IndexArrays(**{**a.__dict__, "targets": a.targets.copy()})
+    bad.targets[3, 0] = a.n
+    with pytest.raises(RuntimeError, match="edge target out of range"):
+        pag.PagIndex.from_arrays(bad)
+    bad = pag.IndexArrays(**{**a.__dict__, "padded_dim": a.padded_dim + 1})
+    with pytest.raises(RuntimeError, match="padded_dim mismatch on load"):
+        pag.PagIndex.from_arrays(bad)
+    ok = pag.PagIndex.from_arrays(a)  # and the untouched arrays still load
+    assert ok.n == a.n
+    ok.close()
