@@ -19,8 +19,9 @@
 //         expansion and the test is monotone in it, so this set is a
 //         superset of the reference's passes);
 //   (ii)  __ballot_sync compaction of the survivors;
-//   (iii) their exact distances (rows prefetched to L2 by bulk copy, streamed
-//         in 128-float chunks with one chunk of look-ahead);
+//   (iii) their exact distances (rows prefetched to L2 by bulk copy; warp-tree
+//         mode: two rows per pass, all loads of a row pair in flight;
+//         reference order: chain-interleaved row copy, 8 rows per batch);
 //   (iv)  an in-order replay re-evaluating the PRT with the live radius
 //         before marking and admitting / pushing to R_F.
 //
