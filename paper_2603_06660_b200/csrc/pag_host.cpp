@@ -739,6 +739,11 @@ Plan make_plan(const pag_gpu_index& ix, const Replica& r, const pag_search_param
     // outgrow any on-chip table and a small one keeps occupancy (with b <= 32
     // the full table stays faster at every efS: cfg-2 efS 300 8.2 vs 8.6 ms)
     L.hash_log2 = (p.efS <= 200 || L.b <= 32) ? 10 : 8;
+    // reference-order searches past efS = 100 with the register working set:
+    // the marks outgrow 768 slots (efS 200: construction search 7.73 -> 7.52 ms,
+    // cfg-2 5.62 -> 5.52 ms with 2048 slots); that mode has no staging buffer,
+    // so the larger table still leaves 4 blocks per SM
+    if (p.exact_dist && L.b <= 32 && p.efS > 100 && 4 * ix.dstride + 4 * ix.L * 16 <= 5 * 1024) L.hash_log2 = 11;
     if (kn.hash_log2 >= 0) L.hash_log2 = static_cast<uint32_t>(kn.hash_log2);
     L.hash_log2 = std::max(3u, std::min(16u, L.hash_log2));  // >= 2 buckets of 4 slots
     {

@@ -1163,7 +1163,15 @@ __device__ void dist_exact_x(const SearchLaunch& P, Common& c, uint32_t items, u
 #pragma unroll
             for (int i = 0; i < LA; ++i)
                 if (NLN ? (i < NLN) : (static_cast<uint32_t>(i) < nln)) buf[i] = ldg_f8(rp + 32 * i);
+            // the construction kernels (PES) are the largest (143 KB of SASS, 23% of
+            // their stall samples wait for instructions): there the line loop stays
+            // rolled, 6 lines per iteration (7.32 vs 7.64 ms per 10k nodes); the query
+            // kernels run it fully unrolled (cfg-2: 2.26 vs 2.37 ms rolled)
+#if PAG_PES
+#pragma unroll 1
+#else
 #pragma unroll(NLN ? (NLN + LA - 1) / LA : 1)
+#endif
             for (uint32_t l0 = 0; l0 < nln; l0 += LA) {
 #pragma unroll
                 for (int i = 0; i < LA; ++i) {
