@@ -8,7 +8,7 @@ residence, result order after every expansion and end_round, reported as the
 reference's logic_error texts) in both distance modes; every result is also
 compared bit for bit with the oracle (reference order, and the warp-tree
 order), and the conservation rule exact = seeds + passes is checked.
-usage: PAG_GPU_LIB=build/lib_validate.so python tools/fuzz_criterion7.py [queries] > fuzz_criterion7.json"""
+usage: PAG_GPU_LIB=build/lib_validate.so python tests/fuzz_criterion7.py [queries] > fuzz_criterion7.json"""
 import collections
 import json
 import os
